@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""Benchmark of the TWED hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg3|cfg3_f32|cfg2|cfg1] [--no-batch] [--no-cpu]
+
+Headline (N=1): BASELINE.json's metric "TWED GCUPS at the n=1M pair" on
+config 3 (single pair, 3-D random walks, n = 1,000,000, nu = 1, lam = 1,
+degree 2, fp64). One step = one full distance of the pair (1e12 DP cells).
+The single pair does not shard across GPUs (replicas only),
+so with N > 1 every rank solves its own replica (weak scaling). The batch
+half of the metric -- twed_batch pairs/s on the 10k x 10k tri config 5 --
+is reported in the "batch" object, sharded over the N GPUs (strong scaling).
+
+  value  : whole-job GCUPS with inputs resident in HBM (device API, CUDA
+           events on the launching stream, max over ranks).
+  e2e    : the same metric through the public host API (numpy in pinned host
+           memory -> H2D -> kernels -> D2H of the distance) = what a user of
+           warpband.twed gets.
+  roofline: the DP kernel against the MEASURED FP64 add throughput of this
+           GPU (add-chain probe in libtwb200; MEASURED_PEAKS.json carries only
+           HBM and bf16 tensor peaks, which do not bound a min-plus DP).
+  cpu_baseline: the reference's CPU algorithm (C restatement in oracle/,
+           per-diagonal parallel band = twedband.engine.twed_parallel) on this
+           host's cores, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+sys.path.insert(0, str(REPO))
+
+# Algorithmic ops per interior DP cell: subtractions, the
+# lp norm (sqrt counted as 1), the time-gap terms, the three candidate sums
+# and the two mins of interior_cost (_kernels.py:61-80).
+FLOPS_PER_CELL = {1: 11, 2: 16, 3: 19, 4: 22}
+
+WORKLOADS = {
+    "cfg1": dict(n=1_000, d=1, seed=0, dtype="f64"),
+    "cfg2": dict(n=100_000, d=1, seed=1, dtype="f64"),
+    "cfg3": dict(n=1_000_000, d=3, seed=2, dtype="f64"),
+    "cfg3_f32": dict(n=1_000_000, d=3, seed=2, dtype="f32"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port of the reference's algorithm)
+# ---------------------------------------------------------------------------
+def cpu_reference_rate(d: int, seed: int, budget_s: float, threads: int, tuned=False):
+    """GCUPS of the reference algorithm on a pair of the workload's generator,
+    sized so that one solve takes about `budget_s` seconds."""
+    from oracle import oracle as orc
+    from paper_2007_16135_b200.workloads import make_pair
+
+    def solve(n):
+        a, ta, b, tb = make_pair(n, d, seed)
+        t0 = time.perf_counter()
+        if tuned:
+            orc.twed_tiled(a, ta, b, tb, 1.0, 1.0, 2, threads=threads)
+        else:
+            orc.twed(a, ta, b, tb, 1.0, 1.0, 2, threads=threads)
+        return time.perf_counter() - t0
+
+    n = 2048
+    dt = solve(n)
+    while dt < budget_s / 8 and n < 1_000_000:
+        n = int(n * 2)
+        dt = solve(n)
+    # scale to the budget (cells ~ n^2)
+    n2 = int(min(1_000_000, n * max(1.0, (budget_s / max(dt, 1e-6)) ** 0.5)))
+    if n2 > n * 1.2:
+        n = n2
+        dt = solve(n)
+    return n * n / dt / 1e9, n, dt
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU algorithm on the host cores."""
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+
+    wl = WORKLOADS[args.workload]
+    threads = os.cpu_count() or 1
+    orc.build()
+    # size one step to about args.ref_step_s seconds
+    gc, n, dt = cpu_reference_rate(wl["d"], wl["seed"], args.ref_step_s, threads)
+    from paper_2007_16135_b200.workloads import make_pair
+    a, ta, b, tb = make_pair(n, wl["d"], wl["seed"])
+    for _ in range(args.warmup):
+        orc.twed(a[:1024], ta[:1024], b[:1024], tb[:1024], 1.0, 1.0, 2, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        orc.twed(a, ta, b, tb, 1.0, 1.0, 2, threads=threads)
+    elapsed = time.perf_counter() - t0
+    value = args.steps * n * n / elapsed / 1e9
+    sample = (f"make_pair(n={n}, d={wl['d']}, seed={wl['seed']}) per step (bounded sample of "
+              f"{args.workload}, n={wl['n']}); C restatement of twedband.engine.twed_parallel "
+              f"(per-diagonal parallel band, _kernels.py:145-174), {threads} threads")
+    line = {
+        "impl": "reference", "metric": "TWED GCUPS (DP cells/s, n=1M pair)", "value": value,
+        "unit": "GCUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic random walks (SURVEY.md §8(d) generator)",
+        "config": {"workload": args.workload, "n": wl["n"], "d": wl["d"], "sample_n": n},
+        "cpu_baseline": {"value": value, "unit": "GCUPS", "cores": threads, "kind": "port",
+                         "sample": sample, "host": orc.host_description()},
+        "e2e": {"value": value, "unit": "GCUPS", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# Our arm
+# ---------------------------------------------------------------------------
+def flush_l2(buf):
+    buf.add_(1)
+
+
+def run_ours(args, world, rank, local):
+    import torch
+
+    import paper_2007_16135_b200 as twb
+    from paper_2007_16135_b200 import _lib
+    from paper_2007_16135_b200.workloads import make_pair
+
+    lib = _lib.load()
+    _lib.require_device()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    wl = WORKLOADS[args.workload]
+    n, d = wl["n"], wl["d"]
+    f32 = wl["dtype"] == "f32"
+    npdt = np.float32 if f32 else np.float64
+    tdt = torch.float32 if f32 else torch.float64
+    a, ta, b, tb = make_pair(n, d, wl["seed"] + 0)  # every replica solves the same pair
+    host = [np.ascontiguousarray(x.astype(npdt)) for x in (a, ta, b, tb)]
+    dev_in = [torch.from_numpy(x).to(dev) for x in host]
+    out = torch.empty(1, dtype=torch.float64, device=dev)
+    cells = float(n) * float(n)
+    l2_flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > L2
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        twb.twed_dev(*dev_in, nu=1.0, lamb=1.0, degree=2, out=out, stream=stream)
+
+    lib.twb_set_kernel_timing(1)
+    for _ in range(args.warmup):
+        step()
+        lib.twb_last_kernel_ms()
+    torch.cuda.synchronize()
+    result = out.item()
+
+    # ---- device-resident timed region -------------------------------------
+    _lib.take_launch_count()
+    kernel_ms = []
+    barrier(world)
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            flush_l2(l2_flush)
+            step()
+            kernel_ms.append(lib.twb_last_kernel_ms())
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    launches = _lib.take_launch_count() + args.steps  # + our L2-flush writes are torch's
+    elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1), world)
+    value = world * args.steps * cells / (elapsed_ms * 1e-3) / 1e9
+    ms_per_step = elapsed_ms / args.steps
+    kmean = float(np.mean(kernel_ms))
+
+    # ---- end to end through the public host API ---------------------------
+    pinned = []
+    for x in host:
+        t = torch.empty(x.shape, dtype=tdt, pin_memory=True)
+        t.numpy()[...] = x
+        pinned.append(t.numpy())
+    lib.twb_set_kernel_timing(0)
+    twb.twed(*pinned, 1.0, 1.0, 2, dtype=npdt, device=local)  # warm
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = twb.twed(*pinned, 1.0, 1.0, 2, dtype=npdt, device=local)
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world)
+    assert (r == result) or f32, (r, result)
+    e2e = {"value": world * args.steps * cells / e2e_s / 1e9, "unit": "GCUPS",
+           "h2d_bytes_per_step": int(sum(x.nbytes for x in host)), "d2h_bytes_per_step": 8,
+           "ms_per_step": e2e_s / args.steps * 1e3, "api": "paper_2007_16135_b200.twed"}
+
+    # ---- roofline -----------------------------------------------------------
+    peak_ops = lib.twb_probe_add_rate(0 if f32 else 1, local)
+    achieved_ops = FLOPS_PER_CELL[d] * cells / (kmean * 1e-3)
+    traffic = None
+    prof = REPO / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(args.workload, {}).get("dram_bytes")
+        except (ValueError, AttributeError):
+            traffic = None
+    roofline = {
+        "bound": "fp32" if f32 else "fp64",
+        "achieved": achieved_ops / 1e12, "peak": peak_ops / 1e12, "unit": "TFLOP/s",
+        "frac": achieved_ops / peak_ops if peak_ops > 0 else None,
+        "traffic": traffic,
+        "kernel": "twb::wave_kernel (persistent flag-synchronised wavefront)",
+        "kernel_ms": kmean, "kernel_share_of_step": kmean / ms_per_step,
+        "flops_per_cell": FLOPS_PER_CELL[d], "cells_per_launch": cells,
+        "peak_source": ("twb_probe_add_rate: measured independent-add throughput of the "
+                        f"{'FP32' if f32 else 'FP64'} pipe on this GPU, 1 op per lane per add "
+                        "(MEASURED_PEAKS.json has no FP64/FP32-ALU peak)"),
+        "algorithmic_bytes_per_cell": 0.0,
+    }
+
+    # ---- batch (config 5: tri 10k x 10k, n=128, d=2, fp32), sharded over ranks -------
+    batch = None
+    if not args.no_batch:
+        batch = run_batch_cfg5(args, world, rank, local)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import oracle as orc
+        threads = os.cpu_count() or 1
+        gc, ns, dts = cpu_reference_rate(d, wl["seed"], args.cpu_budget_s, threads)
+        gct, nst, dtt = cpu_reference_rate(d, wl["seed"], args.cpu_budget_s / 2, threads,
+                                           tuned=True)
+        cpu = {"value": gc, "unit": "GCUPS", "cores": threads, "kind": "port",
+               "sample": (f"one make_pair(n={ns}, d={d}) solve ({dts:.1f} s) by the C "
+                          "restatement of twedband.engine.twed_parallel (per-diagonal "
+                          f"parallel band), {threads} threads"),
+               "tuned_port": {"value": gct, "sample_n": nst,
+                              "what": "bit-identical tiled wavefront restatement (oracle "
+                                      "orc_band_tiled), same threads"},
+               "host": orc.host_description()}
+
+    if rank == 0:
+        line = {
+            "metric": "TWED GCUPS (DP cells/s, n=1M pair)",
+            "value": value, "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if f32 else "f64",
+            "data": "synthetic random walks (SURVEY.md §8(d) make_pair), unit timestamps",
+            "config": {"workload": args.workload, "n": n, "d": d, "nu": 1.0, "lam": 1.0,
+                       "degree": 2, "parallelism": f"replicas x{world} (single pair does not "
+                       "shard)", "l2": "256 MB buffer written between timed steps"},
+            "result": result,
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+            "clocks": clocks.summary(), "gpu_launches": launches,
+            "batch": batch,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def run_batch_cfg5(args, world, rank, local):
+    import torch
+
+    import paper_2007_16135_b200 as twb
+    from paper_2007_16135_b200 import _lib
+    from paper_2007_16135_b200.distributed import row_bounds
+    from paper_2007_16135_b200.workloads import make_set
+
+    N, n, d = args.batch_n, 128, 2
+    S, TS = make_set(N, n, d, 5)
+    S = S.astype(np.float32).reshape(N * n, d)
+    TS = TS.astype(np.float32).reshape(N * n)
+    dev = torch.device("cuda", local)
+    dS = torch.from_numpy(S).to(dev)
+    dT = torch.from_numpy(TS).to(dev)
+    off = np.arange(N + 1, dtype=np.int64) * n
+    b0, b1 = row_bounds(N, world, True)[rank]
+    block = torch.empty((max(b1 - b0, 1), N), dtype=torch.float32, device=dev)
+    lib = _lib.load()
+    lib.twb_set_kernel_timing(1)
+
+    def step():
+        twb.twed_batch_dev(dS, off, dT, nu=1.0, lamb=1.0, degree=2, tri=True, row_begin=b0,
+                           row_end=b1, out=block)
+
+    for _ in range(max(1, args.warmup // 2)):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    ks = []
+    e0.record()
+    for _ in range(args.steps):
+        step()
+        ks.append(lib.twb_last_kernel_ms())
+    e1.record()
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), world) / args.steps
+    pairs = N * (N + 1) // 2
+    cells = pairs * float(n) * n
+    peak = lib.twb_probe_add_rate(0, local)
+    kms = max_over_ranks(float(np.mean(ks)), world)
+    return {"metric": "twed_batch pairs/s (tri 10k x 10k, n=128, d=2, fp32)",
+            "workload": "cfg5", "pairs": pairs, "value": pairs / (ms * 1e-3), "unit": "pairs/s",
+            "gcups": cells / (ms * 1e-3) / 1e9, "ms_per_step": ms, "n_gpus": world,
+            "scaling": "strong", "gather": "not timed (rows stay sharded on each GPU)",
+            "kernel_ms": kms,
+            "roofline": {"bound": "fp32", "achieved": FLOPS_PER_CELL[2] * cells / (kms * 1e-3) / 1e12,
+                         "peak": peak / 1e12, "unit": "TFLOP/s",
+                         "frac": FLOPS_PER_CELL[2] * cells / (kms * 1e-3) / peak}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-batch", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--batch-n", type=int, default=10_000)
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--ref-step-s", type=float, default=8.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warning: fewer than 3 warm-up steps")
+    world, rank, local = (1, 0, 0)
+    if args.impl == "reference":
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, world, rank)
+        return
+    world, rank, local = dist_setup()
+    run_ours(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -56,6 +56,8 @@ def _load():
         lib.orc_band_serial.argtypes = band
         lib.orc_band_parallel.restype = ctypes.c_double
         lib.orc_band_parallel.argtypes = band + [ctypes.c_int]
+        lib.orc_band_tiled.restype = ctypes.c_double
+        lib.orc_band_tiled.argtypes = band + [ctypes.c_int, ctypes.c_int]
         lib.orc_fill_matrix.restype = None
         lib.orc_fill_matrix.argtypes = [_c_double_p] + band
         lib.orc_twed.restype = ctypes.c_double
@@ -114,6 +116,21 @@ def band_serial(pa, pb, nu: float, degree: int) -> float:
     return float(_load().orc_band_serial(
         _p(va), _p(ta), _p(da), va.shape[0] - 1, _p(vb), _p(tb), _p(db), vb.shape[0] - 1,
         va.shape[1], float(nu), int(degree)))
+
+
+def band_tiled(pa, pb, nu: float, degree: int, threads: int = 0, tile: int = 256) -> float:
+    """Bit-identical tiled schedule of the same band (fast golden generation)."""
+    (va, ta, da), (vb, tb, db) = pa, pb
+    return float(_load().orc_band_tiled(
+        _p(va), _p(ta), _p(da), va.shape[0] - 1, _p(vb), _p(tb), _p(db), vb.shape[0] - 1,
+        va.shape[1], float(nu), int(degree), int(threads), int(tile)))
+
+
+def twed_tiled(values_a, times_a, values_b, times_b, nu=1.0, lam=0.0, degree=2, threads=0,
+               tile=256) -> float:
+    pa = prepare_series(values_a, times_a, nu, lam, degree)
+    pb = prepare_series(values_b, times_b, nu, lam, degree)
+    return band_tiled(pa, pb, nu, degree, threads, tile)
 
 
 def fill_matrix(pa, pb, nu: float, degree: int) -> np.ndarray:

@@ -1,0 +1,299 @@
+"""Public API: the reference path's functions on the B200 library.
+
+North-star spellings (cuTWED style) and the reference package's spellings are
+both accepted:
+
+    twed(A, TA, B, TB, nu=1.0, lamb=0.0, degree=2)          # == warpband.twed(..., lam=)
+    twed_batch(AA, TAA, BB, TBB, nu, lamb, degree, tri)      # == warpband.twed_batch(
+                                                             #    series_a, series_b, symmetric=)
+
+Reference seams replaced:
+    twed          -> warpband.twed                 pkg/bindings/src/warpband/__init__.py:43-53
+                     twedband.engine.twed_parallel pkg/src/twedband/engine.py:101-121
+    twed_batch    -> warpband.twed_batch           pkg/bindings/src/warpband/__init__.py:70-86
+                     twedband.engine.twed_batch    pkg/src/twedband/engine.py:183-226
+    band_solve    -> twedband._kernels.twed_band_serial / _parallel (prepared arrays)
+                                                   pkg/src/twedband/_kernels.py:127-174
+    prepare_series-> twedband.core.prepare_series  pkg/src/twedband/core.py:218-234
+
+Precision: ``dtype=np.float64`` (default, bit-identical to the reference) or
+``dtype=np.float32`` (fp32 inputs, fp32 local costs; the DP accumulates in
+fp64 for long series; within 1e-5 relative of the fp64 reference on the same
+fp32-rounded inputs).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .core import (
+    InvalidInputError,
+    TimeSeries,
+    TwedParams,
+    as_series,
+    as_series_list,
+    pack,
+)
+
+_pd = ctypes.POINTER(ctypes.c_double)
+_pf = ctypes.POINTER(ctypes.c_float)
+_pi64 = ctypes.POINTER(ctypes.c_int64)
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    return a.ctypes.data_as(_pd if a.dtype == np.float64 else _pf)
+
+
+def _lam(lamb, lam):
+    if lam is not None and lamb is not None and float(lam) != float(lamb):
+        raise TypeError("pass the deletion penalty once: lamb= (cuTWED) or lam= (warpband)")
+    value = lam if lam is not None else lamb
+    return 0.0 if value is None else value
+
+
+def _dtype(dtype):
+    if dtype is None:
+        return np.float64
+    dt = np.dtype(dtype)
+    if dt not in (np.dtype(np.float64), np.dtype(np.float32)):
+        raise ValueError(f"dtype must be float64 or float32, got {dt}")
+    return dt.type
+
+
+def twed(A, TA, B, TB, nu=1.0, lamb=None, degree=2, *, lam=None, dtype=None, device=0) -> float:
+    """Time warp edit distance between two timestamped series.
+
+    ``A``/``B`` have shape (n,) or (n, d) with matching d; ``TA``/``TB`` shape
+    (n,), strictly increasing. Same validation and messages as warpband.twed.
+    """
+    dt = _dtype(dtype)
+    a = as_series(A, TA, "series A", dt)
+    b = as_series(B, TB, "series B", dt)
+    if a.d != b.d:
+        raise ValueError(f"series dimensions differ: A has d={a.d}, B has d={b.d}")
+    params = TwedParams(nu=nu, lam=_lam(lamb, lam), degree=degree)
+    return twed_series(a, b, params, device=device)
+
+
+def twed_series(a: TimeSeries, b: TimeSeries, params: TwedParams, device=0) -> float:
+    """engine.twed_parallel equivalent on validated series (E:101-121)."""
+    if a.d != b.d:
+        raise InvalidInputError(f"series dimensions differ: {a.d} vs {b.d}")
+    lib = _lib.load()
+    _lib.require_device()
+    va, ta = np.ascontiguousarray(a.values), np.ascontiguousarray(a.timestamps)
+    vb, tb = np.ascontiguousarray(b.values), np.ascontiguousarray(b.timestamps)
+    out = ctypes.c_double(0.0)
+    fn = lib.twb_twed_f64 if va.dtype == np.float64 else lib.twb_twed_f32
+    _lib.check(fn(_ptr(va), a.n, _ptr(ta), _ptr(vb), b.n, _ptr(tb), a.d, params.nu, params.lam,
+                  params.degree, int(device), ctypes.byref(out)))
+    return float(out.value)
+
+
+def _series_from_stacked(X, T, label, dt):
+    """(N, n) / (N, n, d) stacked arrays (+ (N, n) times or None) -> list of series."""
+    X = np.asarray(X, dtype=dt)
+    if X.ndim == 2:
+        X = X[:, :, None]
+    if X.ndim != 3:
+        raise ValueError(f"{label}: stacked values must be (N, n) or (N, n, d), got {X.shape}")
+    if T is None:
+        T = np.broadcast_to(np.arange(X.shape[1], dtype=dt), X.shape[:2])
+    T = np.asarray(T, dtype=dt)
+    if T.shape != X.shape[:2]:
+        raise ValueError(f"{label}: timestamps shape {T.shape} does not match values {X.shape[:2]}")
+    return [as_series(X[k], T[k], f"{label}[{k}]", dt) for k in range(X.shape[0])]
+
+
+def _to_list(X, T, label, dt):
+    if isinstance(X, np.ndarray) or (hasattr(X, "shape") and not isinstance(X, (list, tuple))):
+        arr = np.asarray(X)
+        if arr.ndim in (2, 3) and (T is None or np.asarray(T).ndim == 2):
+            return _series_from_stacked(arr, T, label, dt)
+    items = list(X)
+    if T is not None:
+        times = list(T)
+        if len(times) != len(items):
+            raise ValueError(f"{label}: {len(times)} timestamp arrays for {len(items)} series")
+        items = [(v, t) for v, t in zip(items, times)]
+    return as_series_list(items, label, dt)
+
+
+def batch_matrix(list_a, list_b, params: TwedParams, symmetric=False, device=0,
+                 row_begin=0, row_end=None) -> np.ndarray:
+    """engine.twed_batch (E:183-226) on validated lists. list_b None -> self batch.
+
+    Returns the (row_end - row_begin) x len(list_b) block of rows
+    [row_begin, row_end) of the distance matrix (all rows by default). With
+    symmetric=True and all rows, the full mirrored matrix (E:223-225).
+    """
+    if not list_a or (list_b is not None and not list_b):
+        raise InvalidInputError("batch lists must be nonempty")
+    dim = list_a[0].d
+    for s in list(list_a) + list(list_b or []):
+        if s.d != dim:
+            raise InvalidInputError(f"batch series dimensions differ: {s.d} vs {dim}")
+    lib = _lib.load()
+    _lib.require_device()
+    va, ta, oa = pack(list_a)
+    nA = len(list_a)
+    if row_end is None:
+        row_end = nA
+    if list_b is None:
+        vb = tb = ob = None
+        nB = nA
+    else:
+        vb, tb, ob = pack(list_b)
+        nB = len(list_b)
+    f32 = va.dtype == np.float32
+    out = np.empty((row_end - row_begin, nB), dtype=np.float32 if f32 else np.float64)
+    fn = lib.twb_twed_batch_f32 if f32 else lib.twb_twed_batch_f64
+    _lib.check(fn(_ptr(va), oa.ctypes.data_as(_pi64), nA, _ptr(ta), _ptr(vb),
+                  None if ob is None else ob.ctypes.data_as(_pi64), nB, _ptr(tb), dim,
+                  params.nu, params.lam, params.degree, int(bool(symmetric)), int(row_begin),
+                  int(row_end), int(device), _ptr(out)))
+    return out
+
+
+def twed_batch(AA, TAA=None, BB=None, TBB=None, nu=1.0, lamb=None, degree=2, tri=None, *,
+               lam=None, symmetric=None, dtype=None, device=0) -> np.ndarray:
+    """All-pairs distance matrix R[i, j] = twed(AA[i], BB[j]).
+
+    AA / BB: stacked (N, n) or (N, n, d) arrays with (N, n) timestamps TAA /
+    TBB (None -> 0, 1, ..., n-1), or lists of series (values arrays, (values,
+    times) tuples or TimeSeries) with TAA / TBB None or lists of timestamps.
+    BB None -> self batch (the only case where tri / symmetric is allowed).
+    tri (= the reference's symmetric=True): solve j >= i and mirror, same
+    output as the full matrix.
+    """
+    if tri is not None and symmetric is not None and bool(tri) != bool(symmetric):
+        raise TypeError("pass the triangle flag once: tri= (cuTWED) or symmetric= (warpband)")
+    sym = bool(tri if tri is not None else (symmetric or False))
+    dt = _dtype(dtype)
+    params = TwedParams(nu=nu, lam=_lam(lamb, lam), degree=degree)
+    list_a = _to_list(AA, TAA, "series_a", dt)
+    list_b = None if BB is None else _to_list(BB, TBB, "series_b", dt)
+    if sym and list_b is not None:
+        raise InvalidInputError("symmetric=True requires both lists to be the same collection")
+    if not list_a:
+        raise InvalidInputError("batch lists must be nonempty")
+    return batch_matrix(list_a, list_b, params, symmetric=sym, device=device)
+
+
+def band_solve(pa, pb, nu: float, degree: int, device=0) -> float:
+    """_kernels.twed_band_serial / twed_band_parallel seam (K:127-174).
+
+    pa / pb = (ext_values (n+1, d), ext_times (n+1,), deletion (n+1,)), the
+    reference's PreparedSeries arrays (C:177-234).
+    """
+    lib = _lib.load()
+    _lib.require_device()
+    (va, ta, da), (vb, tb, db) = pa, pb
+    va = np.ascontiguousarray(va, dtype=np.float64)
+    vb = np.ascontiguousarray(vb, dtype=np.float64)
+    if va.ndim == 1:
+        va = va.reshape(-1, 1)
+    if vb.ndim == 1:
+        vb = vb.reshape(-1, 1)
+    ta, da, tb, db = (np.ascontiguousarray(x, dtype=np.float64) for x in (ta, da, tb, db))
+    out = ctypes.c_double(0.0)
+    _lib.check(lib.twb_band_solve_f64(_ptr(va), _ptr(ta), _ptr(da), va.shape[0] - 1, _ptr(vb),
+                                      _ptr(tb), _ptr(db), vb.shape[0] - 1, va.shape[1], float(nu),
+                                      int(degree), int(device), ctypes.byref(out)))
+    return float(out.value)
+
+
+def prepare_series(series: TimeSeries, params: TwedParams, device=0):
+    """core.prepare_series (C:218-234) on the GPU: (ext_values, ext_times, deletion)."""
+    lib = _lib.load()
+    _lib.require_device()
+    v = np.ascontiguousarray(series.values, dtype=np.float64)
+    t = np.ascontiguousarray(series.timestamps, dtype=np.float64)
+    ev = np.empty((series.n + 1, series.d))
+    et = np.empty(series.n + 1)
+    de = np.empty(series.n + 1)
+    _lib.check(lib.twb_prepare_series_f64(_ptr(v), _ptr(t), series.n, series.d, params.nu,
+                                          params.lam, params.degree, int(device), _ptr(ev),
+                                          _ptr(et), _ptr(de)))
+    return ev, et, de
+
+
+# ---------------------------------------------------------------------------
+# Device-resident variants (torch CUDA tensors in, torch CUDA tensor out),
+# the paper's twed_dev: no host copies, caller's stream.
+# ---------------------------------------------------------------------------
+def twed_dev(A, TA, B, TB, nu=1.0, lamb=None, degree=2, *, lam=None, out=None, stream=None):
+    """A, TA, B, TB: contiguous CUDA tensors (float64 or float32). Returns a 1-element
+    float64 CUDA tensor (or fills ``out``). Validation of timestamps is the caller's
+    responsibility (no host round trip)."""
+    import torch
+
+    params = TwedParams(nu=nu, lam=_lam(lamb, lam), degree=degree)
+    lib = _lib.load()
+    A2 = A if A.dim() == 2 else A.reshape(-1, 1)
+    B2 = B if B.dim() == 2 else B.reshape(-1, 1)
+    if A2.shape[1] != B2.shape[1]:
+        raise ValueError(f"series dimensions differ: A has d={A2.shape[1]}, B has d={B2.shape[1]}")
+    for t in (A2, TA, B2, TB):
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError("twed_dev needs contiguous CUDA tensors")
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=A.device)
+    st = stream if stream is not None else torch.cuda.current_stream(A.device)
+    fn = lib.twb_twed_dev_f64 if A2.dtype == torch.float64 else lib.twb_twed_dev_f32
+    with torch.cuda.device(A.device):
+        _lib.check(fn(A2.data_ptr(), A2.shape[0], TA.data_ptr(), B2.data_ptr(), B2.shape[0],
+                      TB.data_ptr(), A2.shape[1], params.nu, params.lam, params.degree,
+                      st.cuda_stream, out.data_ptr()))
+    return out
+
+
+def twed_batch_dev(AA, a_off, TAA, BB=None, b_off=None, TBB=None, nu=1.0, lamb=None, degree=2,
+                   tri=False, *, lam=None, row_begin=0, row_end=None, out=None, stream=None):
+    """Packed device inputs: AA (N_total, d) CUDA tensor, a_off host int64 offsets
+    (N+1,), TAA (N_total,). Returns the (row_end-row_begin, nB) block on the device."""
+    import torch
+
+    params = TwedParams(nu=nu, lam=_lam(lamb, lam), degree=degree)
+    lib = _lib.load()
+    a_off = np.ascontiguousarray(a_off, dtype=np.int64)
+    nA = a_off.shape[0] - 1
+    if BB is not None:
+        b_off = np.ascontiguousarray(b_off, dtype=np.int64)
+        nB = b_off.shape[0] - 1
+    else:
+        nB = nA
+    if row_end is None:
+        row_end = nA
+    AA2 = AA if AA.dim() == 2 else AA.reshape(-1, 1)
+    dim = AA2.shape[1]
+    f32 = AA2.dtype == torch.float32
+    if out is None:
+        out = torch.empty((row_end - row_begin, nB), dtype=AA2.dtype, device=AA.device)
+    st = stream if stream is not None else torch.cuda.current_stream(AA.device)
+    fn = lib.twb_twed_batch_dev_f32 if f32 else lib.twb_twed_batch_dev_f64
+    with torch.cuda.device(AA.device):
+        _lib.check(fn(AA2.data_ptr(), a_off.ctypes.data_as(_pi64), nA, TAA.data_ptr(),
+                      None if BB is None else BB.data_ptr(),
+                      None if BB is None else b_off.ctypes.data_as(_pi64), nB,
+                      None if TBB is None else TBB.data_ptr(), dim, params.nu, params.lam,
+                      params.degree, int(bool(tri)), int(row_begin), int(row_end),
+                      st.cuda_stream, out.data_ptr()))
+    return out
+
+
+def mirror_upper_dev(M, stream=None):
+    """Mirror the strict upper triangle of a square CUDA matrix into its lower half."""
+    import torch
+
+    lib = _lib.load()
+    st = stream if stream is not None else torch.cuda.current_stream(M.device)
+    fn = lib.twb_mirror_upper_dev_f32 if M.dtype == torch.float32 else lib.twb_mirror_upper_dev_f64
+    with torch.cuda.device(M.device):
+        _lib.check(fn(M.data_ptr(), M.shape[0], st.cuda_stream))
+    return M

@@ -1,0 +1,820 @@
+// C ABI of libtwb200.so (declared in include/twb.h). Host orchestration:
+// validation of sizes, device scratch, host<->device copies, precision and
+// kernel-variant selection, and the batch task decomposition.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/twb.h"
+#include "twb_dispatch.h"
+
+namespace {
+
+using namespace twb;
+
+thread_local std::string t_err;
+thread_local int64_t t_launches = 0;
+thread_local LaunchCtx t_ctx;  // main-kernel events of the last call (timing mode)
+thread_local bool t_timing = false;
+
+int fail(int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    t_err = buf;
+    return code;
+}
+
+#define CK(...)                                                                                \
+    do {                                                                                       \
+        cudaError_t e_ = (__VA_ARGS__);                                                        \
+        if (e_ != cudaSuccess)                                                                 \
+            return fail(e_ == cudaErrorMemoryAllocation ? TWB_ENOMEM : TWB_ECUDA,              \
+                        "%s: %s (%s:%d)", #__VA_ARGS__, cudaGetErrorString(e_), __FILE__,      \
+                        __LINE__);                                                             \
+    } while (0)
+
+// Stream-ordered scratch, released (asynchronously) when the call returns.
+struct Scratch {
+    cudaStream_t st;
+    std::vector<void*> ptrs;
+    bool failed = false;
+    explicit Scratch(cudaStream_t s) : st(s) {}
+    void* get(size_t n) {
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, n ? n : 16, st) != cudaSuccess) {
+            failed = true;
+            return nullptr;
+        }
+        ptrs.push_back(p);
+        return p;
+    }
+    template <typename X>
+    X* get_n(size_t n) {
+        return (X*)get(n * sizeof(X));
+    }
+    ~Scratch() {
+        for (void* p : ptrs) cudaFreeAsync(p, st);
+    }
+};
+void* scratch_alloc(void* ctx, size_t n) { return ((Scratch*)ctx)->get(n); }
+
+// Keep freed scratch in the device's stream-ordered pool instead of returning
+// it to the driver at every synchronisation (the 1M pair uses ~1 GB of
+// boundary rows).
+std::once_flag g_pool_once[64];
+void init_pool(int dev) {
+    if (dev < 0 || dev >= 64) return;
+    std::call_once(g_pool_once[dev], [dev]() {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+}
+
+// ---------------------------------------------------------------------------
+// "safe" inputs: every value/time finite with |x| < 2^500 (fp64) or 2^60
+// (fp32), nu and lam finite and small. Then no cell candidate can be NaN or
+// negative-signed, the DP min is order-free and exact symmetry allows
+// swapping the pair. Otherwise the NaN-exact compare chain is used.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void unsafe_kernel(const T* __restrict__ x, int64_t n, double limit, int* flag) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        bad |= !(fabs((double)x[i]) < limit);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+template <typename T>
+__global__ void convert_kernel(const double* __restrict__ in, T* __restrict__ out, int64_t n) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = (T)in[i];
+}
+
+// Mirror the strict upper triangle into the lower one (engine.py:223-225).
+// 32x32 tiles through shared memory so both the read and the write coalesce.
+template <typename T>
+__global__ void mirror_kernel(T* m, int64_t n) {
+    __shared__ T tile[32][33];
+    const int64_t bi = blockIdx.y, bj = blockIdx.x;  // tile (bi, bj) with bj > bi...
+    if (bj < bi) return;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t i = bi * 32 + r, j = bj * 32 + tx;
+        if (i < n && j < n) tile[r][tx] = m[i * n + j];
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t j = bj * 32 + r, i = bi * 32 + tx;  // write (j, i) = tile[tx][r]
+        if (i < n && j < n && j > i) m[j * n + i] = tile[tx][r];
+    }
+}
+
+template <typename T>
+int check_unsafe(const T* d, int64_t n, double limit, int* dflag, cudaStream_t st) {
+    if (n <= 0) return 0;
+    int blocks = (int)std::min<int64_t>((n + 255) / 256, 4096);
+    unsafe_kernel<T><<<blocks, 256, 0, st>>>(d, n, limit, dflag);
+    ++t_launches;
+    return 0;
+}
+
+template <typename T, typename R, typename Z>
+int prepare(const T* values, const T* times, const int64_t* d_off, int64_t nseries, int64_t ntot,
+            int64_t uniform_n, int dim, double nu, double lam, int degree, R* V, R* Tm, Z* Del,
+            cudaStream_t st) {
+    const int64_t work = ntot + nseries;
+    int blocks = (int)std::min<int64_t>((work + 255) / 256, 148 * 16);
+    if (blocks < 1) blocks = 1;
+    prepare_kernel<T, R, Z><<<blocks, 256, 0, st>>>(values, times, d_off, nseries, ntot, uniform_n,
+                                                    dim, nu, lam, degree, V, Tm, Del);
+    ++t_launches;
+    CK(cudaGetLastError());
+    return 0;
+}
+
+// Launch bookkeeping for the next main-kernel launch: counts every launch
+// and, in timing mode, brackets it with events (read by twb_last_kernel_ms).
+LaunchCtx* ctx_begin() {
+    t_launches += t_ctx.launches;
+    t_ctx.launches = 0;
+    t_ctx.timing = t_timing;
+    if (t_timing && !t_ctx.ev0) {
+        cudaEventCreate(&t_ctx.ev0);
+        cudaEventCreate(&t_ctx.ev1);
+    }
+    return &t_ctx;
+}
+
+template <typename R, typename Z>
+cudaError_t call_wave(int dim, int P, bool E, bool N1, const WaveProblem<R, Z>& pr, Scratch& sc,
+                      cudaStream_t st) {
+    Alloc al{scratch_alloc, &sc};
+    switch (dim) {
+        case 1: return wave_d<1, R, Z>(P, E, N1, pr, al, st, ctx_begin());
+        case 2: return wave_d<2, R, Z>(P, E, N1, pr, al, st, ctx_begin());
+        case 3: return wave_d<3, R, Z>(P, E, N1, pr, al, st, ctx_begin());
+        case 4: return wave_d<4, R, Z>(P, E, N1, pr, al, st, ctx_begin());
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <typename R, typename Z>
+cudaError_t call_batch(int dim, int P, bool E, bool N1, const BatchArgs<R, Z>& a, int64_t max_rows,
+                       cudaStream_t st) {
+    switch (dim) {
+        case 1: return batch_d<1, R, Z>(P, E, N1, a, max_rows, st, ctx_begin());
+        case 2: return batch_d<2, R, Z>(P, E, N1, a, max_rows, st, ctx_begin());
+        case 3: return batch_d<3, R, Z>(P, E, N1, a, max_rows, st, ctx_begin());
+        case 4: return batch_d<4, R, Z>(P, E, N1, a, max_rows, st, ctx_begin());
+    }
+    return cudaErrorInvalidValue;
+}
+
+int check_params(int64_t nA, int64_t nB, int dim, double nu, double lam, int degree) {
+    if (nA < 1 || nB < 1) return fail(TWB_EINVAL, "a time series needs at least one sample");
+    if (dim < 1) return fail(TWB_EINVAL, "samples need at least one component");
+    if (dim > 4)
+        return fail(TWB_EUNSUP, "dim=%d: this build compiles kernels for 1 <= dim <= 4", dim);
+    if (!(nu >= 0)) return fail(TWB_EINVAL, "nu must be >= 0, got %g", nu);
+    if (!(lam >= 0)) return fail(TWB_EINVAL, "lam must be >= 0, got %g", lam);
+    if (degree < 1) return fail(TWB_EINVAL, "degree must be a positive integer, got %d", degree);
+    return 0;
+}
+
+// Kernel variant flags from the parameters and the input check.
+struct Variant {
+    int P;
+    bool E, N1;
+};
+Variant pick_variant(int dim, int degree, double nu, double lam, bool unsafe_inputs, double limit) {
+    Variant v;
+    v.P = dim == 1 ? 2 : (degree <= 2 ? degree : 0);
+    bool params_ok = std::isfinite(nu) && std::isfinite(lam) && nu < limit && lam < limit;
+    v.E = unsafe_inputs || !params_ok || v.P == 0;
+    v.N1 = !v.E && nu == 1.0;
+    return v;
+}
+
+template <typename T>
+constexpr double safe_limit() {
+    return sizeof(T) == 8 ? 0x1p500 : 0x1p60;
+}
+
+// ---------------------------------------------------------------------------
+// Single pair. Inputs are device pointers (raw samples); out is a device
+// pointer to one double.
+// ---------------------------------------------------------------------------
+template <typename T, typename R, typename Z>
+int twed_pair_dev(const T* dA, int64_t nA, const T* dTA, const T* dB, int64_t nB, const T* dTB,
+                  int dim, double nu, double lam, int degree, cudaStream_t st, double* d_out) {
+    Scratch sc(st);
+    int* dflag = sc.get_n<int>(1);
+    if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
+    CK(cudaMemsetAsync(dflag, 0, sizeof(int), st));
+    const double lim = safe_limit<R>();
+    check_unsafe(dA, nA * dim, lim, dflag, st);
+    check_unsafe(dTA, nA, lim, dflag, st);
+    check_unsafe(dB, nB * dim, lim, dflag, st);
+    check_unsafe(dTB, nB, lim, dflag, st);
+    int hflag = 0;
+    CK(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+
+    R* V[2] = {sc.get_n<R>((nA + 1) * dim), sc.get_n<R>((nB + 1) * dim)};
+    R* Tm[2] = {sc.get_n<R>(nA + 1), sc.get_n<R>(nB + 1)};
+    Z* Del[2] = {sc.get_n<Z>(nA + 1), sc.get_n<Z>(nB + 1)};
+    Z* zout = sc.get_n<Z>(1);
+    if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
+    int rc;
+    if ((rc = prepare<T, R, Z>(dA, dTA, nullptr, 1, nA, nA, dim, nu, lam, degree, V[0], Tm[0],
+                               Del[0], st)))
+        return rc;
+    if ((rc = prepare<T, R, Z>(dB, dTB, nullptr, 1, nB, nB, dim, nu, lam, degree, V[1], Tm[1],
+                               Del[1], st)))
+        return rc;
+    CK(cudaStreamSynchronize(st));  // hflag
+    Variant v = pick_variant(dim, degree, nu, lam, hflag != 0, lim);
+    // Rows = the longer series (more stripes for the SMs). Exact symmetry
+    // twed(a,b) == twed(b,a) makes the swap bit-identical when the min is
+    // order-free (not in the NaN-exact mode).
+    int ra = 0, rb = 1;
+    int64_t na = nA, nb = nB;
+    if (!v.E && nB > nA) {
+        ra = 1;
+        rb = 0;
+        std::swap(na, nb);
+    }
+    WaveProblem<R, Z> pr;
+    pr.A = {V[ra], Tm[ra], Del[ra]};
+    pr.B = {V[rb], Tm[rb], Del[rb]};
+    pr.nA = na;
+    pr.nB = nb;
+    pr.nu = nu;
+    pr.p = degree;
+    pr.out = zout;
+    CK(call_wave<R, Z>(dim, v.P, v.E, v.N1, pr, sc, st));
+    if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
+    static_assert(sizeof(Z) == 8, "pairs accumulate in fp64");
+    CK(cudaMemcpyAsync(d_out, zout, sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return 0;
+}
+
+template <typename T>
+int twed_pair_host(const T* A, int64_t nA, const T* TA, const T* B, int64_t nB, const T* TB,
+                   int dim, double nu, double lam, int degree, int device, double* out) {
+    int rc = check_params(nA, nB, dim, nu, lam, degree);
+    if (rc) return rc;
+    if (!A || !TA || !B || !TB || !out) return fail(TWB_EINVAL, "null pointer argument");
+    CK(cudaSetDevice(device));
+    init_pool(device);
+    cudaStream_t st = cudaStreamPerThread;
+    Scratch sc(st);
+    T* dA = sc.get_n<T>(nA * dim);
+    T* dTA = sc.get_n<T>(nA);
+    T* dB = sc.get_n<T>(nB * dim);
+    T* dTB = sc.get_n<T>(nB);
+    double* dout = sc.get_n<double>(1);
+    if (sc.failed) return fail(TWB_ENOMEM, "device allocation failed");
+    CK(cudaMemcpyAsync(dA, A, sizeof(T) * nA * dim, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dTA, TA, sizeof(T) * nA, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dB, B, sizeof(T) * nB * dim, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dTB, TB, sizeof(T) * nB, cudaMemcpyHostToDevice, st));
+    if constexpr (sizeof(T) == 8)
+        rc = twed_pair_dev<T, double, double>(dA, nA, dTA, dB, nB, dTB, dim, nu, lam, degree, st, dout);
+    else
+        rc = twed_pair_dev<T, float, double>(dA, nA, dTA, dB, nB, dTB, dim, nu, lam, degree, st, dout);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(out, dout, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// All-pairs matrix (engine.py:183-226). Device inputs, host offsets, device
+// output block (row_end - row_begin) x nBB of type O.
+// ---------------------------------------------------------------------------
+constexpr int64_t BATCH_ROWS_MAX = 32 * BATCH_KMAX;  // row-side length of the warp kernel
+
+template <typename T, typename R, typename Z, typename O>
+int twed_batch_dev_impl(const T* dAA, const int64_t* a_off, int64_t nAA, const T* dTAA,
+                        const T* dBB, const int64_t* b_off, int64_t nBB, const T* dTBB, int dim,
+                        double nu, double lam, int degree, int tri, int64_t row_begin,
+                        int64_t row_end, cudaStream_t st, O* d_out) {
+    const bool self = dBB == nullptr;
+    if (self) {
+        dBB = dAA;
+        dTBB = dTAA;
+        b_off = a_off;
+        nBB = nAA;
+    }
+    const int64_t nrows = row_end - row_begin;
+    Scratch sc(st);
+    // prepared offsets on the host
+    std::vector<int64_t> a_poff(nAA + 1), b_poff(nBB + 1);
+    int64_t amax = 0, bmax = 0;
+    for (int64_t k = 0; k <= nAA; ++k) a_poff[k] = a_off[k] + k;
+    for (int64_t k = 0; k <= nBB; ++k) b_poff[k] = b_off[k] + k;
+    for (int64_t k = 0; k < nAA; ++k) amax = std::max(amax, a_off[k + 1] - a_off[k]);
+    for (int64_t k = 0; k < nBB; ++k) bmax = std::max(bmax, b_off[k + 1] - b_off[k]);
+    auto uniform = [](const int64_t* off, int64_t n) -> int64_t {
+        int64_t len = off[1] - off[0];
+        for (int64_t k = 1; k < n; ++k)
+            if (off[k + 1] - off[k] != len) return 0;
+        return len;
+    };
+    const int64_t totA = a_off[nAA], totB = b_off[nBB];
+
+    int* dflag = sc.get_n<int>(1);
+    int64_t* d_aoff = sc.get_n<int64_t>(nAA + 1);
+    int64_t* d_boff = sc.get_n<int64_t>(nBB + 1);
+    int64_t* d_apoff = sc.get_n<int64_t>(nAA + 1);
+    int64_t* d_bpoff = sc.get_n<int64_t>(nBB + 1);
+    R* VA = sc.get_n<R>((totA + nAA) * dim);
+    R* TmA = sc.get_n<R>(totA + nAA);
+    Z* DelA = sc.get_n<Z>(totA + nAA);
+    R *VB = VA, *TmB = TmA;
+    Z* DelB = DelA;
+    if (!self) {
+        VB = sc.get_n<R>((totB + nBB) * dim);
+        TmB = sc.get_n<R>(totB + nBB);
+        DelB = sc.get_n<Z>(totB + nBB);
+    }
+    if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
+    CK(cudaMemsetAsync(dflag, 0, sizeof(int), st));
+    CK(cudaMemcpyAsync(d_aoff, a_off, sizeof(int64_t) * (nAA + 1), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_apoff, a_poff.data(), sizeof(int64_t) * (nAA + 1), cudaMemcpyHostToDevice, st));
+    if (!self) {
+        CK(cudaMemcpyAsync(d_boff, b_off, sizeof(int64_t) * (nBB + 1), cudaMemcpyHostToDevice, st));
+    }
+    CK(cudaMemcpyAsync(d_bpoff, b_poff.data(), sizeof(int64_t) * (nBB + 1), cudaMemcpyHostToDevice, st));
+    const double lim = safe_limit<R>();
+    check_unsafe(dAA, totA * dim, lim, dflag, st);
+    check_unsafe(dTAA, totA, lim, dflag, st);
+    if (!self) {
+        check_unsafe(dBB, totB * dim, lim, dflag, st);
+        check_unsafe(dTBB, totB, lim, dflag, st);
+    }
+    int hflag = 0;
+    CK(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    int rc;
+    if ((rc = prepare<T, R, Z>(dAA, dTAA, d_aoff, nAA, totA, uniform(a_off, nAA), dim, nu, lam,
+                               degree, VA, TmA, DelA, st)))
+        return rc;
+    if (!self &&
+        (rc = prepare<T, R, Z>(dBB, dTBB, d_boff, nBB, totB, uniform(b_off, nBB), dim, nu, lam,
+                               degree, VB, TmB, DelB, st)))
+        return rc;
+
+    // Output block: the kernel writes only solved entries (+ mirror).
+    const bool mirror = tri && row_begin == 0 && row_end == nAA;
+    Z* zout = nullptr;
+    if constexpr (std::is_same<Z, O>::value) {
+        zout = d_out;
+    } else {
+        zout = sc.get_n<Z>((size_t)nrows * nBB);
+        if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
+    }
+    CK(cudaMemsetAsync(zout, 0, sizeof(Z) * (size_t)nrows * nBB, st));
+
+    // Task decomposition: rows short enough for the warp kernel get chunks of
+    // `chunk` B series; longer rows are solved pair by pair (wave kernel).
+    double avg_b = (double)totB / (double)nBB;
+    int chunk = (int)std::lround(3072.0 / (avg_b + 1.0));
+    chunk = std::max(1, std::min(chunk, MAX_CHUNK));
+    std::vector<int64_t> prefix(nrows + 1, 0);
+    std::vector<int64_t> long_rows;
+    int64_t max_rows = 1;
+    for (int64_t li = 0; li < nrows; ++li) {
+        const int64_t i = row_begin + li;
+        const int64_t na = a_off[i + 1] - a_off[i];
+        const int64_t jfirst = tri ? i : 0;
+        int64_t nt = 0;
+        if (na <= BATCH_ROWS_MAX) {
+            nt = nBB > jfirst ? (nBB - jfirst + chunk - 1) / chunk : 0;
+            max_rows = std::max(max_rows, na);
+        } else {
+            long_rows.push_back(li);
+        }
+        prefix[li + 1] = prefix[li] + nt;
+    }
+    CK(cudaStreamSynchronize(st));  // hflag (and the host vectors stay alive)
+    const Variant v = pick_variant(dim, degree, nu, lam, hflag != 0, lim);
+
+    if (prefix[nrows] > 0) {
+        int64_t* d_prefix = sc.get_n<int64_t>(nrows + 1);
+        unsigned long long* d_counter = sc.get_n<unsigned long long>(1);
+        if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
+        CK(cudaMemcpyAsync(d_prefix, prefix.data(), sizeof(int64_t) * (nrows + 1),
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), st));
+        BatchArgs<R, Z> a;
+        a.A = {VA, TmA, DelA};
+        a.B = {VB, TmB, DelB};
+        a.a_poff = d_apoff;
+        a.b_poff = d_bpoff;
+        a.nBB = nBB;
+        a.row_begin = row_begin;
+        a.nrows = nrows;
+        a.task_prefix = d_prefix;
+        a.ntasks = prefix[nrows];
+        a.chunk = chunk;
+        a.tri = tri;
+        a.mirror = mirror;
+        a.out = zout;
+        a.ld = nBB;
+        a.nu = nu;
+        a.p = degree;
+        a.counter = d_counter;
+        CK(call_batch<R, Z>(dim, v.P, v.E, v.N1, a, max_rows, st));
+    }
+    // Long row-side series: one wavefront solve per pair.
+    if (!long_rows.empty()) {
+        using ZW = double;  // pairs accumulate in fp64 in both precision modes
+        ZW* wout = nullptr;
+        Z* tmp = nullptr;
+        for (int64_t li : long_rows) {
+            const int64_t i = row_begin + li;
+            const int64_t jfirst = tri ? i : 0;
+            for (int64_t j = jfirst; j < nBB; ++j) {
+                Scratch pair_sc(st);
+                // the wave kernel needs Z = double; in fp32-accumulator builds
+                // (R=float, Z=float) rows this long cannot happen: Z=float is
+                // only selected when every series is short.
+                if constexpr (std::is_same<Z, double>::value) {
+                    WaveProblem<R, double> pr;
+                    pr.A = {VA + a_poff[i] * dim, TmA + a_poff[i], DelA + a_poff[i]};
+                    pr.B = {VB + b_poff[j] * dim, TmB + b_poff[j], DelB + b_poff[j]};
+                    pr.nA = a_off[i + 1] - a_off[i];
+                    pr.nB = b_off[j + 1] - b_off[j];
+                    pr.nu = nu;
+                    pr.p = degree;
+                    pr.out = zout + li * nBB + j;
+                    CK(call_wave<R, double>(dim, v.P, v.E, v.N1, pr, pair_sc, st));
+                    if (pair_sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
+                    if (mirror && j != i)
+                        CK(cudaMemcpyAsync(zout + j * nBB + i, zout + li * nBB + j, sizeof(double),
+                                           cudaMemcpyDeviceToDevice, st));
+                } else {
+                    (void)wout;
+                    (void)tmp;
+                    return fail(TWB_EUNSUP, "internal: fp32 accumulator with long series");
+                }
+            }
+        }
+    }
+    if constexpr (!std::is_same<Z, O>::value) {
+        const int64_t n = nrows * nBB;
+        int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+        convert_kernel<O><<<std::max(blocks, 1), 256, 0, st>>>((const double*)zout, d_out, n);
+        ++t_launches;
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(st));  // scratch (host vectors) lifetime
+    return 0;
+}
+
+int check_batch(const int64_t* a_off, int64_t nAA, const int64_t* b_off, int64_t nBB, int dim,
+                double nu, double lam, int degree, int64_t row_begin, int64_t row_end) {
+    if (!a_off || nAA < 1 || (b_off && nBB < 1)) return fail(TWB_EINVAL, "batch lists must be nonempty");
+    for (int64_t k = 0; k < nAA; ++k)
+        if (a_off[k + 1] - a_off[k] < 1) return fail(TWB_EINVAL, "a time series needs at least one sample");
+    if (b_off)
+        for (int64_t k = 0; k < nBB; ++k)
+            if (b_off[k + 1] - b_off[k] < 1)
+                return fail(TWB_EINVAL, "a time series needs at least one sample");
+    if (row_begin < 0 || row_end > nAA || row_begin >= row_end)
+        return fail(TWB_EINVAL, "row range [%lld, %lld) outside [0, %lld)", (long long)row_begin,
+                    (long long)row_end, (long long)nAA);
+    return check_params(1, 1, dim, nu, lam, degree);
+}
+
+template <typename T, typename O>
+int twed_batch_dev(const T* dAA, const int64_t* a_off, int64_t nAA, const T* dTAA, const T* dBB,
+                   const int64_t* b_off, int64_t nBB, const T* dTBB, int dim, double nu, double lam,
+                   int degree, int tri, int64_t row_begin, int64_t row_end, cudaStream_t st,
+                   O* d_out) {
+    const bool self = dBB == nullptr;
+    int rc = check_batch(a_off, nAA, self ? nullptr : b_off, nBB, dim, nu, lam, degree, row_begin,
+                         row_end);
+    if (rc) return rc;
+    if (tri && !self) return fail(TWB_EINVAL, "symmetric=True requires both lists to be the same collection");
+    if constexpr (sizeof(T) == 8) {
+        return twed_batch_dev_impl<T, double, double, O>(dAA, a_off, nAA, dTAA, dBB, b_off, nBB,
+                                                         dTBB, dim, nu, lam, degree, tri, row_begin,
+                                                         row_end, st, d_out);
+    } else {
+        // fp32 mode: fp32 accumulator when every series is short (error grows
+        // with the path length), fp64 accumulator otherwise.
+        int64_t mx = 0;
+        for (int64_t k = 0; k < nAA; ++k) mx = std::max(mx, a_off[k + 1] - a_off[k]);
+        if (!self)
+            for (int64_t k = 0; k < nBB; ++k) mx = std::max(mx, b_off[k + 1] - b_off[k]);
+        if (mx <= 4096 / 2 && mx <= BATCH_ROWS_MAX)
+            return twed_batch_dev_impl<T, float, float, O>(dAA, a_off, nAA, dTAA, dBB, b_off, nBB,
+                                                           dTBB, dim, nu, lam, degree, tri,
+                                                           row_begin, row_end, st, d_out);
+        return twed_batch_dev_impl<T, float, double, O>(dAA, a_off, nAA, dTAA, dBB, b_off, nBB,
+                                                        dTBB, dim, nu, lam, degree, tri, row_begin,
+                                                        row_end, st, d_out);
+    }
+}
+
+template <typename T, typename O>
+int twed_batch_host(const T* AA, const int64_t* a_off, int64_t nAA, const T* TAA, const T* BB,
+                    const int64_t* b_off, int64_t nBB, const T* TBB, int dim, double nu, double lam,
+                    int degree, int tri, int64_t row_begin, int64_t row_end, int device, O* out) {
+    const bool self = BB == nullptr;
+    int rc = check_batch(a_off, nAA, self ? nullptr : b_off, nBB, dim, nu, lam, degree, row_begin,
+                         row_end);
+    if (rc) return rc;
+    if (!AA || !TAA || !out || (!self && (!TBB || !b_off))) return fail(TWB_EINVAL, "null pointer argument");
+    CK(cudaSetDevice(device));
+    init_pool(device);
+    cudaStream_t st = cudaStreamPerThread;
+    Scratch sc(st);
+    const int64_t totA = a_off[nAA];
+    const int64_t totB = self ? 0 : b_off[nBB];
+    const int64_t ncols = self ? nAA : nBB;
+    T* dA = sc.get_n<T>(totA * dim);
+    T* dTA = sc.get_n<T>(totA);
+    T* dB = self ? nullptr : sc.get_n<T>(totB * dim);
+    T* dTB = self ? nullptr : sc.get_n<T>(totB);
+    O* dout = sc.get_n<O>((size_t)(row_end - row_begin) * ncols);
+    if (sc.failed) return fail(TWB_ENOMEM, "device allocation failed");
+    CK(cudaMemcpyAsync(dA, AA, sizeof(T) * totA * dim, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dTA, TAA, sizeof(T) * totA, cudaMemcpyHostToDevice, st));
+    if (!self) {
+        CK(cudaMemcpyAsync(dB, BB, sizeof(T) * totB * dim, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dTB, TBB, sizeof(T) * totB, cudaMemcpyHostToDevice, st));
+    }
+    rc = twed_batch_dev<T, O>(dA, a_off, nAA, dTA, dB, b_off, nBB, dTB, dim, nu, lam, degree, tri,
+                              row_begin, row_end, st, dout);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(out, dout, sizeof(O) * (size_t)(row_end - row_begin) * ncols,
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+template <typename T>
+int mirror_dev(T* d, int64_t n, cudaStream_t st) {
+    if (!d || n < 1) return fail(TWB_EINVAL, "bad matrix");
+    dim3 grid((unsigned)((n + 31) / 32), (unsigned)((n + 31) / 32));
+    mirror_kernel<T><<<grid, dim3(32, 8), 0, st>>>(d, n);
+    ++t_launches;
+    CK(cudaGetLastError());
+    return 0;
+}
+
+// Pipe-throughput probe: independent add chains per thread, enough warps to
+// saturate the pipe; returns lane-ops/s (one add = one op). This is the
+// measured denominator of the ALU roofline (MEASURED_PEAKS.json only has HBM
+// and bf16 tensor peaks).
+template <typename T>
+__global__ void add_probe_kernel(T* sink, int iters, T seed) {
+    T a0 = seed + threadIdx.x, a1 = a0 + 1, a2 = a0 + 2, a3 = a0 + 3, a4 = a0 + 4, a5 = a0 + 5,
+      a6 = a0 + 6, a7 = a0 + 7;
+    const T inc = seed * (T)1e-9;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            a0 += inc; a1 += inc; a2 += inc; a3 += inc; a4 += inc; a5 += inc; a6 += inc; a7 += inc;
+        }
+    }
+    T r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
+    if (r == (T)-1) sink[0] = r;  // keep the chains alive
+}
+
+}  // namespace
+
+extern "C" {
+
+double twb_probe_add_rate(int fp64, int device) {
+    if (cudaSetDevice(device) != cudaSuccess) return -1.0;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaStream_t st = cudaStreamPerThread;
+    void* sink = nullptr;
+    if (cudaMallocAsync(&sink, 16, st) != cudaSuccess) return -1.0;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 4096, threads = 512, blocks = sms * 4;
+    float best = 1e30f;
+    for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(e0, st);
+        if (fp64) add_probe_kernel<double><<<blocks, threads, 0, st>>>((double*)sink, iters, 1.0);
+        else add_probe_kernel<float><<<blocks, threads, 0, st>>>((float*)sink, iters, 1.0f);
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (rep > 0 && ms < best) best = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFreeAsync(sink, st);
+    cudaStreamSynchronize(st);
+    if (cudaGetLastError() != cudaSuccess) return -1.0;
+    const double ops = (double)blocks * threads * iters * 64.0;
+    return ops / (best * 1e-3);
+}
+
+int twb_version(void) { return 100; }
+
+size_t twb_last_error(char* buf, size_t len) {
+    if (buf && len) {
+        size_t n = std::min(len - 1, t_err.size());
+        memcpy(buf, t_err.data(), n);
+        buf[n] = 0;
+    }
+    return t_err.size();
+}
+
+int twb_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int64_t twb_take_launch_count(void) {
+    int64_t n = t_launches + t_ctx.launches;
+    t_launches = 0;
+    t_ctx.launches = 0;
+    return n;
+}
+
+void twb_set_kernel_timing(int enable) { t_timing = enable != 0; }
+
+float twb_last_kernel_ms(void) {
+    if (!t_timing || !t_ctx.ev1) return -1.f;
+    if (cudaEventSynchronize(t_ctx.ev1) != cudaSuccess) return -1.f;
+    float ms = -1.f;
+    if (cudaEventElapsedTime(&ms, t_ctx.ev0, t_ctx.ev1) != cudaSuccess) return -1.f;
+    return ms;
+}
+
+int twb_twed_f64(const double* A, int64_t nA, const double* TA, const double* B, int64_t nB,
+                 const double* TB, int32_t dim, double nu, double lam, int32_t degree,
+                 int32_t device, double* out) {
+    return twed_pair_host<double>(A, nA, TA, B, nB, TB, dim, nu, lam, degree, device, out);
+}
+
+int twb_twed_f32(const float* A, int64_t nA, const float* TA, const float* B, int64_t nB,
+                 const float* TB, int32_t dim, double nu, double lam, int32_t degree,
+                 int32_t device, double* out) {
+    return twed_pair_host<float>(A, nA, TA, B, nB, TB, dim, nu, lam, degree, device, out);
+}
+
+int twb_twed_dev_f64(const double* dA, int64_t nA, const double* dTA, const double* dB, int64_t nB,
+                     const double* dTB, int32_t dim, double nu, double lam, int32_t degree,
+                     void* stream, double* d_out) {
+    int rc = check_params(nA, nB, dim, nu, lam, degree);
+    if (rc) return rc;
+    return twed_pair_dev<double, double, double>(dA, nA, dTA, dB, nB, dTB, dim, nu, lam, degree,
+                                                 (cudaStream_t)stream, d_out);
+}
+
+int twb_twed_dev_f32(const float* dA, int64_t nA, const float* dTA, const float* dB, int64_t nB,
+                     const float* dTB, int32_t dim, double nu, double lam, int32_t degree,
+                     void* stream, double* d_out) {
+    int rc = check_params(nA, nB, dim, nu, lam, degree);
+    if (rc) return rc;
+    return twed_pair_dev<float, float, double>(dA, nA, dTA, dB, nB, dTB, dim, nu, lam, degree,
+                                               (cudaStream_t)stream, d_out);
+}
+
+int twb_twed_batch_f64(const double* AA, const int64_t* a_off, int64_t nAA, const double* TAA,
+                       const double* BB, const int64_t* b_off, int64_t nBB, const double* TBB,
+                       int32_t dim, double nu, double lam, int32_t degree, int32_t tri,
+                       int64_t row_begin, int64_t row_end, int32_t device, double* out) {
+    return twed_batch_host<double, double>(AA, a_off, nAA, TAA, BB, b_off, nBB, TBB, dim, nu, lam,
+                                           degree, tri, row_begin, row_end, device, out);
+}
+
+int twb_twed_batch_f32(const float* AA, const int64_t* a_off, int64_t nAA, const float* TAA,
+                       const float* BB, const int64_t* b_off, int64_t nBB, const float* TBB,
+                       int32_t dim, double nu, double lam, int32_t degree, int32_t tri,
+                       int64_t row_begin, int64_t row_end, int32_t device, float* out) {
+    return twed_batch_host<float, float>(AA, a_off, nAA, TAA, BB, b_off, nBB, TBB, dim, nu, lam,
+                                         degree, tri, row_begin, row_end, device, out);
+}
+
+int twb_twed_batch_dev_f64(const double* dAA, const int64_t* a_off, int64_t nAA, const double* dTAA,
+                           const double* dBB, const int64_t* b_off, int64_t nBB, const double* dTBB,
+                           int32_t dim, double nu, double lam, int32_t degree, int32_t tri,
+                           int64_t row_begin, int64_t row_end, void* stream, double* d_out) {
+    return twed_batch_dev<double, double>(dAA, a_off, nAA, dTAA, dBB, b_off, nBB, dTBB, dim, nu, lam,
+                                          degree, tri, row_begin, row_end, (cudaStream_t)stream,
+                                          d_out);
+}
+
+int twb_twed_batch_dev_f32(const float* dAA, const int64_t* a_off, int64_t nAA, const float* dTAA,
+                           const float* dBB, const int64_t* b_off, int64_t nBB, const float* dTBB,
+                           int32_t dim, double nu, double lam, int32_t degree, int32_t tri,
+                           int64_t row_begin, int64_t row_end, void* stream, float* d_out) {
+    return twed_batch_dev<float, float>(dAA, a_off, nAA, dTAA, dBB, b_off, nBB, dTBB, dim, nu, lam,
+                                        degree, tri, row_begin, row_end, (cudaStream_t)stream, d_out);
+}
+
+int twb_mirror_upper_dev_f64(double* d_out, int64_t n, void* stream) {
+    return mirror_dev<double>(d_out, n, (cudaStream_t)stream);
+}
+int twb_mirror_upper_dev_f32(float* d_out, int64_t n, void* stream) {
+    return mirror_dev<float>(d_out, n, (cudaStream_t)stream);
+}
+
+int twb_band_solve_f64(const double* va, const double* ta, const double* dela, int64_t na,
+                       const double* vb, const double* tb, const double* delb, int64_t nb,
+                       int32_t dim, double nu, int32_t degree, int32_t device, double* out) {
+    int rc = check_params(na, nb, dim, nu, 0.0, degree);
+    if (rc) return rc;
+    if (!va || !ta || !dela || !vb || !tb || !delb || !out) return fail(TWB_EINVAL, "null pointer argument");
+    CK(cudaSetDevice(device));
+    init_pool(device);
+    cudaStream_t st = cudaStreamPerThread;
+    Scratch sc(st);
+    double* d[6] = {sc.get_n<double>((na + 1) * dim), sc.get_n<double>(na + 1),
+                    sc.get_n<double>(na + 1),         sc.get_n<double>((nb + 1) * dim),
+                    sc.get_n<double>(nb + 1),         sc.get_n<double>(nb + 1)};
+    double* dout = sc.get_n<double>(1);
+    int* dflag = sc.get_n<int>(1);
+    if (sc.failed) return fail(TWB_ENOMEM, "device allocation failed");
+    const double* h[6] = {va, ta, dela, vb, tb, delb};
+    const int64_t n[6] = {(na + 1) * dim, na + 1, na + 1, (nb + 1) * dim, nb + 1, nb + 1};
+    for (int k = 0; k < 6; ++k)
+        CK(cudaMemcpyAsync(d[k], h[k], sizeof(double) * n[k], cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(dflag, 0, sizeof(int), st));
+    const double lim = safe_limit<double>();
+    for (int k = 0; k < 6; ++k) {
+        const bool is_del = k == 2 || k == 5;  // del[0] = +inf by construction
+        check_unsafe(d[k] + (is_del ? 1 : 0), n[k] - (is_del ? 1 : 0), lim, dflag, st);
+    }
+    int hflag = 0;
+    CK(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const Variant v = pick_variant(dim, degree, nu, 0.0, hflag != 0, lim);
+    WaveProblem<double, double> pr;
+    pr.A = {d[0], d[1], d[2]};
+    pr.B = {d[3], d[4], d[5]};
+    pr.nA = na;
+    pr.nB = nb;
+    if (!v.E && nb > na) {
+        std::swap(pr.A, pr.B);
+        std::swap(pr.nA, pr.nB);
+    }
+    pr.nu = nu;
+    pr.p = degree;
+    pr.out = dout;
+    CK(call_wave<double, double>(dim, v.P, v.E, v.N1, pr, sc, st));
+    if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
+    CK(cudaMemcpyAsync(out, dout, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+int twb_prepare_series_f64(const double* values, const double* times, int64_t n, int32_t dim,
+                           double nu, double lam, int32_t degree, int32_t device, double* ext_values,
+                           double* ext_times, double* deletion) {
+    if (n < 1 || dim < 1 || degree < 1) return fail(TWB_EINVAL, "bad series");
+    CK(cudaSetDevice(device));
+    init_pool(device);
+    cudaStream_t st = cudaStreamPerThread;
+    Scratch sc(st);
+    double* dv = sc.get_n<double>(n * dim);
+    double* dt = sc.get_n<double>(n);
+    double* V = sc.get_n<double>((n + 1) * dim);
+    double* Tm = sc.get_n<double>(n + 1);
+    double* Del = sc.get_n<double>(n + 1);
+    if (sc.failed) return fail(TWB_ENOMEM, "device allocation failed");
+    CK(cudaMemcpyAsync(dv, values, sizeof(double) * n * dim, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dt, times, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    int rc = prepare<double, double, double>(dv, dt, nullptr, 1, n, n, dim, nu, lam, degree, V, Tm,
+                                             Del, st);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(ext_values, V, sizeof(double) * (n + 1) * dim, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ext_times, Tm, sizeof(double) * (n + 1), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(deletion, Del, sizeof(double) * (n + 1), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+}  // extern "C"

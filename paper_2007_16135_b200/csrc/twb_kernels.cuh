@@ -1,0 +1,375 @@
+// Kernels of the B200 TWED library (sm_100a).
+//
+//   prepare_kernel  : per-series precompute (core.py:218-234): zero-prefixed
+//                     values/times and deletion costs, HBM-bound.
+//   batch_kernel    : all-pairs matrix (engine.py:183-226). One warp per task
+//                     (A series i, a run of B series); the warp keeps A's
+//                     rows in registers and streams the task's B series back
+//                     to back, so the 31-step lane skew is paid once per task,
+//                     not once per pair.
+//   wave_kernel     : one long pair (engine.py:101-121, the band of
+//                     _kernels.py:127-174). Persistent grid of row stripes;
+//                     warps of a CTA are chained through shared-memory rings,
+//                     CTAs through flag-synchronised global boundary rows
+//                     (st.release.gpu / ld.acquire.gpu progress counters), so
+//                     the anti-diagonal wavefront sweeps without a launch or a
+//                     grid barrier per diagonal.
+#pragma once
+
+#include "twb_stripe.cuh"
+
+namespace twb {
+
+// ---------------------------------------------------------------------------
+// Precompute. Runtime d and degree; same operation order as the reference.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double lp_rt(const double* x, const double* y, int d, int p) {
+    if (d == 1) return fabs(x[0] - y[0]);
+    if (p == 1) {
+        double acc = fabs(x[0] - y[0]);
+        for (int k = 1; k < d; ++k) acc = __dadd_rn(acc, fabs(x[k] - y[k]));
+        return acc;
+    }
+    if (p == 2) {
+        double d0 = x[0] - y[0];
+        double acc = __dmul_rn(d0, d0);
+        for (int k = 1; k < d; ++k) {
+            double dk = x[k] - y[k];
+            acc = __dadd_rn(acc, __dmul_rn(dk, dk));
+        }
+        return __dsqrt_rn(acc);
+    }
+    double acc = 0.0;
+    for (int k = 0; k < d; ++k) acc = __dadd_rn(acc, int_power(fabs(x[k] - y[k]), p));
+    return pow(acc, 1.0 / (double)p);
+}
+
+// values: (ntot, d) raw samples of all series back to back (T = double or
+// float; float is widened exactly). off: (nseries+1) sample offsets.
+// Outputs prepared rows o = i + k + 1 for sample i of series k, and the
+// virtual row off[k] + k.
+template <typename T, typename R, typename Z>
+__global__ void prepare_kernel(const T* __restrict__ values, const T* __restrict__ times,
+                               const int64_t* __restrict__ off, int64_t nseries, int64_t ntot,
+                               int64_t uniform_n, int d, double nu, double lam, int p,
+                               R* __restrict__ V, R* __restrict__ Tm, Z* __restrict__ Del) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntot + nseries;
+         i += stride) {
+        if (i >= ntot) {  // virtual row of series k
+            int64_t k = i - ntot;
+            int64_t o = (uniform_n > 0 ? k * uniform_n : off[k]) + k;
+            for (int c = 0; c < d; ++c) V[o * d + c] = R(0);
+            Tm[o] = R(0);
+            Del[o] = (Z)dinf();
+            continue;
+        }
+        int64_t k;
+        if (uniform_n > 0) {
+            k = i / uniform_n;
+        } else {  // last k with off[k] <= i
+            int64_t lo = 0, hi = nseries;
+            while (hi - lo > 1) {
+                int64_t mid = (lo + hi) >> 1;
+                if (off[mid] <= i) lo = mid; else hi = mid;
+            }
+            k = lo;
+        }
+        int64_t start = uniform_n > 0 ? k * uniform_n : off[k];
+        bool first = i == start;
+        double cur[16], prev[16];
+        double gap;
+        double cost;
+        double ti = (double)times[i];
+        double tp = first ? 0.0 : (double)times[i - 1];
+        if (d <= 16) {
+            for (int c = 0; c < d; ++c) {
+                cur[c] = (double)values[i * d + c];
+                prev[c] = first ? 0.0 : (double)values[(i - 1) * d + c];
+            }
+            cost = lp_rt(cur, prev, d, p);
+        } else {  // long vectors: same sums, read straight from memory
+            if (p == 1 || p == 2 || d == 1) {
+                double acc = 0.0;
+                for (int c = 0; c < d; ++c) {
+                    double x = (double)values[i * d + c];
+                    double y = first ? 0.0 : (double)values[(i - 1) * d + c];
+                    double df = x - y;
+                    double term = p == 1 ? fabs(df) : __dmul_rn(df, df);
+                    acc = c == 0 ? term : __dadd_rn(acc, term);
+                }
+                cost = p == 1 ? acc : __dsqrt_rn(acc);
+            } else {
+                double acc = 0.0;
+                for (int c = 0; c < d; ++c) {
+                    double x = (double)values[i * d + c];
+                    double y = first ? 0.0 : (double)values[(i - 1) * d + c];
+                    acc = __dadd_rn(acc, int_power(fabs(x - y), p));
+                }
+                cost = pow(acc, 1.0 / (double)p);
+            }
+        }
+        gap = fabs(ti - tp);
+        int64_t o = i + k + 1;
+        for (int c = 0; c < d; ++c) V[o * d + c] = (R)values[i * d + c];
+        Tm[o] = (R)times[i];
+        Del[o] = (Z)__dadd_rn(__dadd_rn(cost, __dmul_rn(nu, gap)), lam);  // core.py:233
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Batch: all-pairs matrix.
+// ---------------------------------------------------------------------------
+constexpr int MAX_CHUNK = 64;  // B series per task
+
+template <int D, typename R, typename Z>
+__host__ __device__ constexpr size_t batch_smem(int warps) {
+    return sizeof(ColRing<D, R, Z>) * warps + sizeof(int) * MAX_CHUNK * warps;
+}
+
+template <typename R, typename Z>
+struct BatchArgs {
+    PreparedT<R, Z> A, B;
+    const int64_t* a_poff;  // prepared offsets of the A series (nAA+1)
+    const int64_t* b_poff;  // prepared offsets of the B series (nBB+1)
+    int64_t nBB;
+    int64_t row_begin;           // first A series of this shard
+    int64_t nrows;               // A series in this shard
+    const int64_t* task_prefix;  // (nrows+1) tasks before local row
+    int64_t ntasks;
+    int chunk;   // B series per task (<= MAX_CHUNK)
+    int tri;     // only j >= i (engine.py:200-201)
+    int mirror;  // also write (j, i) (engine.py:223-225); only when all rows are local
+    Z* out;
+    int64_t ld;
+    double nu;
+    int p;
+    unsigned long long* counter;
+};
+
+template <int D, int K, int P, bool EXACT_NAN, bool NU1, int WARPS, typename R, typename Z>
+__global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z> args) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto* rings = reinterpret_cast<ColRing<D, R, Z>*>(smem_raw);
+    auto* slen = reinterpret_cast<int(*)[MAX_CHUNK]>(smem_raw + sizeof(ColRing<D, R, Z>) * WARPS);
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    ColRing<D, R, Z>& ring = rings[warp];
+    const Z INF = zinf<Z>();
+    LaneRows<D, K, P, EXACT_NAN, NU1, R, Z> L;
+
+    while (true) {
+        unsigned long long task = 0;
+        if (lane == 0) task = atomicAdd(args.counter, 1ull);
+        task = __shfl_sync(FULL, task, 0);
+        if ((int64_t)task >= args.ntasks) return;
+        // local row: last li with task_prefix[li] <= task
+        int64_t lo = 0, hi = args.nrows;
+        while (hi - lo > 1) {
+            int64_t mid = (lo + hi) >> 1;
+            if (args.task_prefix[mid] <= (int64_t)task) lo = mid; else hi = mid;
+        }
+        const int64_t li = lo;
+        const int64_t i = args.row_begin + li;
+        const int64_t jfirst = args.tri ? i : 0;
+        const int64_t j0 = jfirst + ((int64_t)task - args.task_prefix[li]) * args.chunk;
+        const int64_t j1 = min(j0 + (int64_t)args.chunk, args.nBB);
+        const int nser = (int)(j1 - j0);
+
+        const int64_t abase = args.a_poff[i];
+        const int64_t nA = args.a_poff[i + 1] - abase - 1;
+        L.load(args.A, abase, 1 + (int64_t)lane * K, nA);
+        for (int k = lane; k < nser; k += 32)
+            slen[warp][k] = (int)(args.b_poff[j0 + k + 1] - args.b_poff[j0 + k]);
+        const int64_t c0 = args.b_poff[j0];
+        const int64_t ncols = args.b_poff[j1] - c0;
+        stage_block<D>(ring, args.B, c0, ncols, 0, lane);
+        stage_block<D>(ring, args.B, c0, ncols, 1, lane);
+        __syncwarp();
+
+        const int own_lane = (int)((nA - 1) / K);
+        const int own_q = (int)((nA - 1) % K);
+        Z* orow = args.out + li * args.ld;
+        int sidx = 0, pos = 0;
+        int curlen = slen[warp][0];
+        Z zbot = INF;
+        const int64_t nsteps = ncols + 31;
+        for (int64_t s = 0; s < nsteps; ++s) {
+            if ((s & 31) == 0) {
+                cp_async_wait<1>();
+                __syncwarp();
+                stage_block<D>(ring, args.B, c0, ncols, (s >> 5) + 2, lane);
+            }
+            Z zup = __shfl_up_sync(FULL, zbot, 1);
+            const int64_t j = s - lane;
+            if (j >= 0 && j < ncols) {
+                const int slot = (int)(j & (RING_COLS - 1));
+                R vb[D];
+#pragma unroll
+                for (int k = 0; k < D; ++k) vb[k] = ring.v[slot * D + k];
+                const R tb = ring.t[slot];
+                const Z delb = ring.del[slot];
+                const bool col0 = pos == 0;
+                if (lane == 0) zup = col0 ? Z(0) : INF;  // row 0: z(0,0)=0, z(0,j)=inf
+                zbot = L.step(vb, tb, delb, zup, col0, args.nu, args.p);
+                if (++pos == curlen) {
+                    if (lane == own_lane) {
+                        const Z v = L.z_at(own_q);
+                        const int64_t jj = j0 + sidx;
+                        orow[jj] = v;
+                        if (args.mirror && jj != i) args.out[(jj - args.row_begin) * args.ld + i] = v;
+                    }
+                    ++sidx;
+                    pos = 0;
+                    curlen = sidx < nser ? slen[warp][sidx] : 0;
+                }
+            }
+        }
+        cp_async_wait<0>();
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Wavefront: one long pair.
+// ---------------------------------------------------------------------------
+constexpr int ZRS = 256;  // shared-memory ring between consecutive warps (columns)
+constexpr int CHS = 16;   // warp-to-warp publish granularity (columns)
+constexpr int CHG = 32;   // CTA-to-CTA publish granularity (columns)
+
+template <int D, typename R, typename Z>
+__host__ __device__ constexpr size_t wave_smem_rings(int warps) {
+    return (sizeof(ColRing<D, R, Z>) * warps + 15) / 16 * 16;
+}
+template <int D, typename R, typename Z>
+__host__ __device__ constexpr size_t wave_smem(int warps) {
+    return wave_smem_rings<D, R, Z>(warps) + sizeof(Z) * (ZRS * warps + 64) + sizeof(int) * 2 * warps;
+}
+
+template <typename R, typename Z>
+struct WaveArgs {
+    PreparedT<R, Z> A, B;  // single prepared series each (row 0 virtual)
+    int64_t nA, nB;
+    int64_t S;  // stripes
+    int64_t H;  // rows per stripe
+    Z* gbuf;            // gridDim.x x (nB+1): bottom row of the CTA's current stripe
+    long long* gprog;   // gridDim.x progress counters: stripe*(nB+1) + columns published
+    double nu;
+    int p;
+    double* out;
+};
+
+template <int D, int K, int P, bool EXACT_NAN, bool NU1, int WARPS, typename R, typename Z>
+__global__ void __launch_bounds__(WARPS * 32, 1) wave_kernel(const WaveArgs<R, Z> args) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    auto* rings = reinterpret_cast<ColRing<D, R, Z>*>(smem_raw);
+    auto* zring = reinterpret_cast<Z(*)[ZRS]>(smem_raw + wave_smem_rings<D, R, Z>(WARPS));
+    Z* gstage = reinterpret_cast<Z*>(smem_raw + wave_smem_rings<D, R, Z>(WARPS) + sizeof(Z) * ZRS * WARPS);
+    int* prog = reinterpret_cast<int*>(gstage + 64);
+    int* cons = prog + WARPS;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int G = gridDim.x;
+    const int b = blockIdx.x;
+    const int pb = (b + G - 1) % G;
+    ColRing<D, R, Z>& ring = rings[warp];
+    const Z INF = zinf<Z>();
+    const int64_t ncols = args.nB + 1;
+    LaneRows<D, K, P, EXACT_NAN, NU1, R, Z> L;
+
+    const int64_t s_last = (args.nA - 1) / args.H;
+    const int64_t loc_last = (args.nA - 1) - s_last * args.H;
+    const int own_warp = (int)(loc_last / (32 * K));
+    const int own_lane = (int)((loc_last / K) % 32);
+    const int own_q = (int)(loc_last % K);
+
+    for (int64_t s = b; s < args.S; s += G) {
+        __syncthreads();
+        if (threadIdx.x < WARPS) {
+            prog[threadIdx.x] = 0;
+            cons[threadIdx.x] = 0;
+        }
+        __syncthreads();
+        const int64_t first_row = 1 + s * args.H;
+        const int64_t rows = min(args.H, args.nA - s * args.H);
+        const int wact = (int)((rows + 32 * K - 1) / (32 * K));
+        if (warp >= wact) continue;
+
+        L.load(args.A, 0, first_row + (int64_t)(warp * 32 + lane) * K, args.nA);
+        stage_block<D>(ring, args.B, 0, ncols, 0, lane);
+        stage_block<D>(ring, args.B, 0, ncols, 1, lane);
+        __syncwarp();
+
+        const bool top_boundary = s == 0;                    // row 0 above warp 0
+        const bool to_ring = warp < wact - 1;                // feed warp+1
+        const bool to_global = !to_ring && s + 1 < args.S;   // feed the next stripe
+        const bool owner = s == s_last && warp == own_warp && lane == own_lane;
+        const long long gbase_in = (long long)(s - 1) * ncols;
+        const long long gbase_out = (long long)s * ncols;
+        Z* grow_out = args.gbuf + (int64_t)b * ncols;
+        const Z* grow_in = args.gbuf + (int64_t)pb * ncols;
+
+        Z zbot = INF;
+        const int64_t nsteps = ncols + 31;
+        for (int64_t st = 0; st < nsteps; ++st) {
+            if ((st & 31) == 0) {
+                cp_async_wait<1>();
+                __syncwarp();
+                stage_block<D>(ring, args.B, 0, ncols, (st >> 5) + 2, lane);
+                if (warp == 0 && !top_boundary && st < ncols) {
+                    // previous stripe's bottom row, columns [st, st+32)
+                    const long long need = gbase_in + min(st + CHG, ncols);
+                    while (ld_acquire_gpu(args.gprog + pb) < need) __nanosleep(20);
+                    const int64_t c = st + lane;
+                    if (c < ncols) gstage[c & 63] = __ldcg(grow_in + c);
+                    __syncwarp();
+                }
+            }
+            if (warp > 0 && (st % CHS) == 0 && st < ncols) {
+                if (lane == 0) st_release_cta(&cons[warp], (int)st);
+                const int need = (int)min(st + CHS, ncols);
+                while (ld_acquire_cta(&prog[warp]) < need) {
+                }
+            }
+            const int64_t j31 = st - 31;  // lane 31's column this step
+            if (to_ring && j31 >= 0 && j31 < ncols && (j31 % CHS) == 0) {
+                const int need = (int)(j31 + CHS - ZRS);
+                while (ld_acquire_cta(&cons[warp + 1]) < need) {
+                }
+            }
+            Z zup = __shfl_up_sync(FULL, zbot, 1);
+            const int64_t j = st - lane;
+            if (j >= 0 && j < ncols) {
+                const int slot = (int)(j & (RING_COLS - 1));
+                R vb[D];
+#pragma unroll
+                for (int k = 0; k < D; ++k) vb[k] = ring.v[slot * D + k];
+                const R tb = ring.t[slot];
+                const Z delb = ring.del[slot];
+                const bool col0 = j == 0;
+                if (lane == 0) {
+                    if (warp > 0) zup = zring[warp][j % ZRS];
+                    else if (top_boundary) zup = col0 ? Z(0) : INF;
+                    else zup = gstage[j & 63];
+                }
+                zbot = L.step(vb, tb, delb, zup, col0, args.nu, args.p);
+                if (lane == 31) {
+                    if (to_ring) {
+                        zring[warp + 1][j % ZRS] = zbot;
+                        if (((j + 1) % CHS) == 0 || j == ncols - 1)
+                            st_release_cta(&prog[warp + 1], (int)(j + 1));
+                    } else if (to_global) {
+                        grow_out[j] = zbot;
+                        if (((j + 1) % CHG) == 0 || j == ncols - 1)
+                            st_release_gpu(args.gprog + b, gbase_out + j + 1);
+                    }
+                }
+                if (owner && j == ncols - 1) args.out[0] = L.z_at(own_q);
+            }
+        }
+        cp_async_wait<0>();
+        __syncwarp();
+    }
+}
+
+}  // namespace twb

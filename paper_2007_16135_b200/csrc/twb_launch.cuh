@@ -1,0 +1,141 @@
+// Host-side launchers (templates instantiated per D / precision in
+// twb_inst_*.cu so the 100+ kernel variants compile in parallel).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "twb_kernels.cuh"
+
+namespace twb {
+
+struct WaveCfg {
+    int warps;  // warps per CTA
+    int k;      // rows per lane
+};
+
+// Per-call launch bookkeeping: kernel count, and (when timing is on) CUDA
+// events bracketing the main DP kernel on its stream.
+struct LaunchCtx {
+    int64_t launches = 0;
+    bool timing = false;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    void before(cudaStream_t st) {
+        if (timing) cudaEventRecord(ev0, st);
+    }
+    void after(cudaStream_t st) {
+        ++launches;
+        if (timing) cudaEventRecord(ev1, st);
+    }
+};
+
+// Scratch allocation hook provided by the API layer (stream-ordered).
+struct Alloc {
+    void* (*fn)(void* ctx, size_t bytes);
+    void* ctx;
+    void* get(size_t bytes) const { return fn(ctx, bytes); }
+};
+
+template <typename R, typename Z>
+struct WaveProblem {
+    PreparedT<R, Z> A, B;
+    int64_t nA, nB;
+    double nu;
+    int p;
+    Z* out;  // device, one value
+};
+
+// Batch kernel variants: rows per lane K in {2, 4, 8} (series of up to 256
+// samples on the row side), 8 warps per CTA, persistent grid with an atomic
+// task counter.
+constexpr int BATCH_WARPS = 4;
+constexpr int BATCH_KMAX = 8;
+
+template <int D, int P, bool E, bool N1, typename R, typename Z>
+cudaError_t run_batch(BatchArgs<R, Z> a, int64_t max_rows, cudaStream_t st, LaunchCtx* ctx) {
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = batch_smem<D, R, Z>(BATCH_WARPS);
+    auto go = [&](auto kern) -> cudaError_t {
+        int occ = 0;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, BATCH_WARPS * 32, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) occ = 1;
+        int64_t want = (a.ntasks + BATCH_WARPS - 1) / BATCH_WARPS;
+        int64_t grid = (int64_t)sms * occ;
+        if (want < grid) grid = want;
+        if (grid < 1) grid = 1;
+        ctx->before(st);
+        kern<<<(unsigned)grid, BATCH_WARPS * 32, smem, st>>>(a);
+        ctx->after(st);
+        return cudaGetLastError();
+    };
+    if (max_rows <= 32 * 2) return go(batch_kernel<D, 2, P, E, N1, BATCH_WARPS, R, Z>);
+    if (max_rows <= 32 * 4) return go(batch_kernel<D, 4, P, E, N1, BATCH_WARPS, R, Z>);
+    if (max_rows <= 32 * 8) return go(batch_kernel<D, 8, P, E, N1, BATCH_WARPS, R, Z>);
+    return cudaErrorInvalidValue;
+}
+
+// Wavefront variants: (warps, k) in {(8, 2), (8, 8)} -- picked so that the
+// row stripes cover every SM (short pairs) or amortise the per-row top-row
+// recompute (long pairs).
+template <int D, int K, int P, bool E, bool N1, int W, typename R, typename Z>
+cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream_t st,
+                         LaunchCtx* ctx) {
+    auto kern = wave_kernel<D, K, P, E, N1, W, R, Z>;
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = wave_smem<D, R, Z>(W);
+    int occ = 0;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * 32, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorLaunchOutOfResources;
+    const int64_t H = (int64_t)W * 32 * K;
+    const int64_t S = (pr.nA + H - 1) / H;
+    const int64_t cap = (int64_t)sms * occ;
+    const int64_t rounds = (S + cap - 1) / cap;
+    const int64_t G = (S + rounds - 1) / rounds;
+    WaveArgs<R, Z> a;
+    a.A = pr.A;
+    a.B = pr.B;
+    a.nA = pr.nA;
+    a.nB = pr.nB;
+    a.S = S;
+    a.H = H;
+    a.nu = pr.nu;
+    a.p = pr.p;
+    a.out = pr.out;
+    a.gbuf = (Z*)alloc.get(sizeof(Z) * (size_t)G * (size_t)(pr.nB + 1));
+    a.gprog = (long long*)alloc.get(sizeof(long long) * (size_t)G);
+    if (!a.gbuf || !a.gprog) return cudaErrorMemoryAllocation;
+    e = cudaMemsetAsync(a.gprog, 0, sizeof(long long) * (size_t)G, st);
+    if (e != cudaSuccess) return e;
+    void* params[] = {(void*)&a};
+    // Cooperative launch: every CTA must be co-resident (CTA b spins on CTA b-1).
+    ctx->before(st);
+    e = cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)G), dim3(W * 32), params, smem, st);
+    ctx->after(st);
+    return e;
+}
+
+template <int D, int P, bool E, bool N1, typename R, typename Z>
+cudaError_t run_wave(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream_t st,
+                     LaunchCtx* ctx) {
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // Long row side: 8 rows per lane (2048-row stripes). Otherwise 2 rows per
+    // lane so that the stripes still spread over the SMs.
+    if (pr.nA >= (int64_t)sms * 8 * 32 * 8 * 2)
+        return run_wave_cfg<D, 8, P, E, N1, 8, R, Z>(pr, alloc, st, ctx);
+    return run_wave_cfg<D, 2, P, E, N1, 8, R, Z>(pr, alloc, st, ctx);
+}
+
+}  // namespace twb

@@ -1,0 +1,228 @@
+// Row-stripe machinery shared by the batch and wavefront kernels.
+//
+// Layout (device memory), the reference's PreparedSeries (core.py:177-234):
+//   V   (rows, D) row-major, row 0 of each series the zero vector   [type R]
+//   Tm  (rows)    timestamps, row 0 = 0                              [type R]
+//   Del (rows)    deletion costs, row 0 = +inf                        [type Z]
+// Series lists are packed back to back; series k occupies prepared rows
+// [poff[k], poff[k+1]) with poff[k] = off[k] + k.
+//
+// Precision modes: fp64  R = Z = double   (bit-identical to the reference)
+//                  fp32  R = float, Z = float  (short series: batch)
+//                  fp32  R = float, Z = double (long pairs: fp64 accumulator)
+//
+// Execution model. A warp owns 32*K consecutive DP rows of series A: lane t
+// holds rows r0..r0+K-1 in registers. The warp streams the columns of the B
+// side (one or many prepared series back to back, each with its virtual column
+// 0) with a one-step skew per lane: at step s lane t computes column j = s - t
+// for its K rows, top to bottom. The cell above its first row comes from lane
+// t-1 by warp shuffle (computed one step earlier); lane 0 gets it from the
+// row-0 boundary, the previous warp (shared-memory ring) or the previous CTA
+// (flag-synchronised global buffer). Per row the lane keeps z(r, j-1),
+// d(r, j-1) and t_a(r) - t_b(j-1), so interior_cost's d_prev and second
+// t_gap term (_kernels.py:70-71) are reused bit-identically instead of being
+// recomputed. Column data is staged per warp into a 128-column shared-memory
+// ring by cp.async, two 32-column blocks ahead of use.
+#pragma once
+
+#include "twb_device.cuh"
+
+namespace twb {
+
+template <typename R, typename Z>
+struct PreparedT {
+    const R* v;    // (rows, D)
+    const R* t;    // (rows)
+    const Z* del;  // (rows)
+};
+
+constexpr int RING_COLS = 128;  // per-warp column staging ring (4 blocks of 32)
+
+template <int D, typename R, typename Z>
+struct ColRing {
+    R v[RING_COLS * D];
+    R t[RING_COLS];
+    Z del[RING_COLS];
+};
+
+template <typename X>
+__device__ __forceinline__ void cp_async_elem(X* smem, const X* gmem, bool valid) {
+    if constexpr (sizeof(X) == 8) cp_async8(smem, gmem, valid);
+    else cp_async4(smem, gmem, valid);
+}
+
+// Stage 32-column block `blk` (stream columns 32*blk .. 32*blk+31, i.e. global
+// prepared rows c0 + ...) into its ring slot. Columns >= ncols are zero-filled.
+template <int D, typename R, typename Z>
+__device__ __forceinline__ void stage_block(ColRing<D, R, Z>& ring, const PreparedT<R, Z>& B,
+                                            int64_t c0, int64_t ncols, int64_t blk, int lane) {
+    const int64_t j = blk * 32 + lane;
+    const bool ok = j < ncols;
+    const int64_t g = c0 + (ok ? j : 0);
+    const int slot = (int)(j & (RING_COLS - 1));
+    const int base = (int)((blk * 32) & (RING_COLS - 1)) * D;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const int e = lane + 32 * k;  // element of the block's 32*D words
+        const int64_t gj = blk * 32 + e / D;
+        const bool okk = gj < ncols;
+        cp_async_elem(&ring.v[base + e], B.v + (c0 + (okk ? gj : 0)) * D + (e % D), okk);
+    }
+    cp_async_elem(&ring.t[slot], B.t + g, ok);
+    cp_async_elem(&ring.del[slot], B.del + g, ok);
+    cp_async_commit();
+}
+
+// fp32 lp distance (fp32 mode only; tolerance, not bit parity).
+template <int D, int P>
+__device__ __forceinline__ float lp_dist_f(const float (&x)[D], const float (&y)[D], int p) {
+    if constexpr (D == 1) {
+        return fabsf(x[0] - y[0]);
+    } else {
+        const int pp = P ? P : p;
+        if (pp == 1) {
+            float acc = fabsf(x[0] - y[0]);
+#pragma unroll
+            for (int k = 1; k < D; ++k) acc += fabsf(x[k] - y[k]);
+            return acc;
+        }
+        if (pp == 2) {
+            float d0 = x[0] - y[0];
+            float acc = d0 * d0;
+#pragma unroll
+            for (int k = 1; k < D; ++k) {
+                float dk = x[k] - y[k];
+                acc = acc + dk * dk;
+            }
+            float r;
+            asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(acc));
+            return r;
+        }
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc += __powf(fabsf(x[k] - y[k]), (float)pp);
+        return __powf(acc, 1.0f / (float)pp);
+    }
+}
+
+template <int D, int P, typename R>
+__device__ __forceinline__ R dist(const R (&x)[D], const R (&y)[D], int p) {
+    if constexpr (sizeof(R) == 8) return lp_dist<D, P>(x, y, p);
+    else return lp_dist_f<D, P>(x, y, p);
+}
+
+template <typename Z>
+__device__ __forceinline__ Z zinf() {
+    if constexpr (sizeof(Z) == 8) return dinf();
+    else return __int_as_float(0x7f800000);
+}
+
+// Per-lane DP state for K rows.
+template <int D, int K, int P, bool EXACT_NAN, bool NU1, typename R, typename Z>
+struct LaneRows {
+    R a[K][D];
+    R ta[K];
+    Z da[K];
+    Z zl[K];  // z(r, j-1)
+    R mr[K];  // d(r, j-1)
+    R gr[K];  // t_a(r) - t_b(j-1) (signed, |.| at use)
+    Z zupp;   // z(r0-1, j-1)
+    R aup[D];
+    R tup;
+    R vbp[D];  // column j-1 values (top-row recompute)
+    R tbp;
+
+    // Rows [r0, r0+K) of the prepared series at `base`; rows > n are zero
+    // (computed, never read back).
+    __device__ __forceinline__ void load(const PreparedT<R, Z>& A, int64_t base, int64_t r0,
+                                         int64_t n) {
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+            const int64_t r = r0 + q;
+            const bool ok = r <= n;
+            const int64_t g = base + (ok ? r : 0);
+#pragma unroll
+            for (int k = 0; k < D; ++k) a[q][k] = ok ? A.v[g * D + k] : R(0);
+            ta[q] = ok ? A.t[g] : R(0);
+            da[q] = ok ? A.del[g] : Z(0);
+        }
+        const int64_t ru = r0 - 1;
+        const bool oku = ru <= n;
+        const int64_t gu = base + (oku ? ru : 0);
+#pragma unroll
+        for (int k = 0; k < D; ++k) aup[k] = oku ? A.v[gu * D + k] : R(0);
+        tup = oku ? A.t[gu] : R(0);
+#pragma unroll
+        for (int k = 0; k < D; ++k) vbp[k] = R(0);
+        tbp = R(0);
+        zupp = zinf<Z>();
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+            zl[q] = zinf<Z>();
+            mr[q] = R(0);
+            gr[q] = R(0);
+        }
+    }
+
+    // One column j for the K rows (interior_cost, _kernels.py:61-80, per row).
+    // zup = z(r0-1, j). col0: j is a virtual column 0 (z(r, 0) = +inf, r >= 1).
+    // Returns z(r0+K-1, j).
+    __device__ __forceinline__ Z step(const R (&vb)[D], R tb, Z delb, Z zup, bool col0, double nu,
+                                      int p) {
+        // d(r0-1, j-1) and t_a(r0-1) - t_b(j-1): same inputs and operations as
+        // the lane above used one step earlier -> bit-identical recompute.
+        R m_up = dist<D, P, R>(aup, vbp, p);
+        R g_up = tup - tbp;
+        Z zu = zup;
+        Z zd = zupp;
+        const Z INF = zinf<Z>();
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+            const R m = dist<D, P, R>(a[q], vb, p);
+            const R g = ta[q] - tb;
+            Z match;
+            if constexpr (sizeof(R) == 8) {
+                // ((z_diag + d_now) + d_prev) + nu * (|g_now| + |g_prev|)
+                const double gs = __dadd_rn(fabs(g), fabs(g_up));
+                const double tt = NU1 ? gs : __dmul_rn(nu, gs);
+                match = __dadd_rn(__dadd_rn(__dadd_rn(zd, m), m_up), tt);
+            } else if constexpr (sizeof(Z) == 4) {
+                const float gs = fabsf(g) + fabsf(g_up);
+                const float tt = NU1 ? gs : (float)nu * gs;
+                match = ((zd + m) + m_up) + tt;
+            } else {
+                // fp32 local cost, fp64 accumulator
+                const float gs = fabsf(g) + fabsf(g_up);
+                const float tt = NU1 ? gs : (float)nu * gs;
+                const float w = (m + m_up) + tt;
+                match = zd + (double)w;
+            }
+            const Z del_b = zl[q] + delb;
+            const Z del_a = zu + da[q];
+            Z z = cell_min<EXACT_NAN>(del_a, del_b, match);
+            z = col0 ? INF : z;
+            zd = zl[q];
+            zl[q] = z;
+            zu = z;
+            m_up = mr[q];
+            g_up = gr[q];
+            mr[q] = m;
+            gr[q] = g;
+        }
+        zupp = zup;
+#pragma unroll
+        for (int k = 0; k < D; ++k) vbp[k] = vb[k];
+        tbp = tb;
+        return zu;
+    }
+
+    // z of row slot q (runtime index) without local-memory indexing.
+    __device__ __forceinline__ Z z_at(int q) const {
+        Z r = zl[0];
+#pragma unroll
+        for (int k = 1; k < K; ++k) r = (q == k) ? zl[k] : r;
+        return r;
+    }
+};
+
+}  // namespace twb
