@@ -20,9 +20,11 @@ is reported in the "batch" object, sharded over the N GPUs (strong scaling).
   roofline: the DP kernel against the MEASURED FP64 add throughput of this
            GPU (add-chain probe in libtwb200; MEASURED_PEAKS.json carries only
            HBM and bf16 tensor peaks, which do not bound a min-plus DP).
-  cpu_baseline: the reference's CPU algorithm (C restatement in oracle/,
-           per-diagonal parallel band = twedband.engine.twed_parallel) on this
-           host's cores, on a bounded sample of the same workload.
+  cpu_baseline: the reference package itself (twedband.engine.twed_parallel
+           from baseline/_ref, numba per-diagonal parallel band, all host
+           cores) on a bounded sample of the same workload, with the C
+           restatement in oracle/ beside it; the port alone when baseline/_ref
+           is absent.
 """
 
 from __future__ import annotations
@@ -45,6 +47,7 @@ sys.path.insert(0, str(REPO))
 # lp norm (sqrt counted as 1), the time-gap terms, the three candidate sums
 # and the two mins of interior_cost (_kernels.py:61-80).
 FLOPS_PER_CELL = {1: 11, 2: 16, 3: 19, 4: 22}
+METRIC = "TWED GCUPS (DP cells/s, n=1M pair)"
 
 WORKLOADS = {
     "cfg1": dict(n=1_000, d=1, seed=0, dtype="f64"),
@@ -154,29 +157,62 @@ def sum_over_ranks(x: float, world: int) -> float:
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (oracle port of the reference's algorithm)
+# CPU reference: the reference package itself (baseline/_ref, installed from
+# /root/reference with pip; travels to the GPU box with the snapshot) and the
+# C restatement in oracle/ (always available) as a second column.
 # ---------------------------------------------------------------------------
-def cpu_reference_rate(d: int, seed: int, budget_s: float, threads: int, tuned=False):
-    """GCUPS of the reference algorithm on a pair of the workload's generator,
-    sized so that one solve takes about `budget_s` seconds."""
-    from oracle import oracle as orc
+def load_reference():
+    """twedband from baseline/_ref, or None when it is not installed / numba is missing."""
+    ref = REPO / "baseline" / "_ref"
+    if not (ref / "twedband").is_dir():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/twb_numba_cache")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import twedband
+        return twedband
+    except Exception as exc:  # numba absent or broken install
+        log(f"reference package unavailable: {exc!r}")
+        return None
+
+
+def _ref_solver(kind: str, d: int, seed: int, threads: int):
+    """solve(n) -> seconds for one pair of the workload generator at length n."""
     from paper_2007_16135_b200.workloads import make_pair
 
-    def solve(n):
-        a, ta, b, tb = make_pair(n, d, seed)
-        t0 = time.perf_counter()
-        if tuned:
-            orc.twed_tiled(a, ta, b, tb, 1.0, 1.0, 2, threads=threads)
-        else:
-            orc.twed(a, ta, b, tb, 1.0, 1.0, 2, threads=threads)
-        return time.perf_counter() - t0
+    if kind == "reference":
+        tb = load_reference()
+        params = tb.TwedParams(1.0, 1.0, 2)
 
+        def solve(n):
+            a, ta, b, tb_ = make_pair(n, d, seed)
+            sa, sb = tb.TimeSeries(a, ta), tb.TimeSeries(b, tb_)
+            t0 = time.perf_counter()
+            tb.twed_parallel(sa, sb, params, threads)
+            return time.perf_counter() - t0
+    else:
+        from oracle import oracle as orc
+        orc.build()
+
+        def solve(n):
+            a, ta, b, tb_ = make_pair(n, d, seed)
+            t0 = time.perf_counter()
+            orc.twed(a, ta, b, tb_, 1.0, 1.0, 2, threads=threads)
+            return time.perf_counter() - t0
+    return solve
+
+
+def cpu_reference_rate(kind: str, d: int, seed: int, budget_s: float, threads: int):
+    """GCUPS of the CPU reference on one pair of the workload's generator,
+    sized so that the final solve takes about `budget_s` seconds (cells ~ n^2)."""
+    solve = _ref_solver(kind, d, seed, threads)
+    solve(600)  # JIT / thread-pool warm-up (parallel path needs n >= 512)
     n = 2048
     dt = solve(n)
-    while dt < budget_s / 8 and n < 1_000_000:
-        n = int(n * 2)
+    while dt < budget_s / 16 and n < 1_000_000:
+        n *= 2
         dt = solve(n)
-    # scale to the budget (cells ~ n^2)
     n2 = int(min(1_000_000, n * max(1.0, (budget_s / max(dt, 1e-6)) ** 0.5)))
     if n2 > n * 1.2:
         n = n2
@@ -184,38 +220,47 @@ def cpu_reference_rate(d: int, seed: int, budget_s: float, threads: int, tuned=F
     return n * n / dt / 1e9, n, dt
 
 
+def reference_kind() -> str:
+    return "reference" if load_reference() is not None else "port"
+
+
+def reference_sample_text(kind, n, d, seed, threads, workload):
+    what = ("twedband.engine.twed_parallel (the reference package from baseline/_ref, numba "
+            "per-diagonal parallel band, _kernels.py:145-174)" if kind == "reference" else
+            "C restatement of twedband.engine.twed_parallel (oracle/twed_oracle.c, per-diagonal "
+            "parallel band)")
+    return (f"one make_pair(n={n}, d={d}, seed={seed}) solve per step (bounded sample of "
+            f"{workload}); {what}, {threads} threads")
+
+
 def run_reference(args, world, rank):
-    """--impl reference: the reference's CPU algorithm on the host cores."""
+    """--impl reference: the reference's CPU implementation on the host cores."""
     if rank != 0:
         return
-    from oracle import oracle as orc
-
     wl = WORKLOADS[args.workload]
     threads = os.cpu_count() or 1
-    orc.build()
-    # size one step to about args.ref_step_s seconds
-    gc, n, dt = cpu_reference_rate(wl["d"], wl["seed"], args.ref_step_s, threads)
-    from paper_2007_16135_b200.workloads import make_pair
-    a, ta, b, tb = make_pair(n, wl["d"], wl["seed"])
+    kind = reference_kind()
+    d, seed = wl["d"], wl["seed"]
+    _, n, _ = cpu_reference_rate(kind, d, seed, args.ref_step_s, threads)
+    solve = _ref_solver(kind, d, seed, threads)
     for _ in range(args.warmup):
-        orc.twed(a[:1024], ta[:1024], b[:1024], tb[:1024], 1.0, 1.0, 2, threads=threads)
-    t0 = time.perf_counter()
+        solve(1024)
+    elapsed = 0.0
     for _ in range(args.steps):
-        orc.twed(a, ta, b, tb, 1.0, 1.0, 2, threads=threads)
-    elapsed = time.perf_counter() - t0
+        elapsed += solve(n)
     value = args.steps * n * n / elapsed / 1e9
-    sample = (f"make_pair(n={n}, d={wl['d']}, seed={wl['seed']}) per step (bounded sample of "
-              f"{args.workload}, n={wl['n']}); C restatement of twedband.engine.twed_parallel "
-              f"(per-diagonal parallel band, _kernels.py:145-174), {threads} threads")
+    from oracle import oracle as orc
     line = {
-        "impl": "reference", "metric": "TWED GCUPS (DP cells/s, n=1M pair)", "value": value,
+        "impl": "reference", "metric": METRIC, "value": value,
         "unit": "GCUPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic random walks (SURVEY.md §8(d) generator)",
-        "config": {"workload": args.workload, "n": wl["n"], "d": wl["d"], "sample_n": n},
-        "cpu_baseline": {"value": value, "unit": "GCUPS", "cores": threads, "kind": "port",
-                         "sample": sample, "host": orc.host_description()},
+        "config": {"workload": args.workload, "n": wl["n"], "d": d, "sample_n": n},
+        "cpu_baseline": {"value": value, "unit": "GCUPS", "cores": threads, "kind": kind,
+                         "sample": reference_sample_text(kind, n, d, seed, threads,
+                                                         args.workload),
+                         "host": orc.host_description()},
         "e2e": {"value": value, "unit": "GCUPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -336,21 +381,21 @@ def run_ours(args, world, rank, local):
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import oracle as orc
         threads = os.cpu_count() or 1
-        gc, ns, dts = cpu_reference_rate(d, wl["seed"], args.cpu_budget_s, threads)
-        gct, nst, dtt = cpu_reference_rate(d, wl["seed"], args.cpu_budget_s / 2, threads,
-                                           tuned=True)
-        cpu = {"value": gc, "unit": "GCUPS", "cores": threads, "kind": "port",
-               "sample": (f"one make_pair(n={ns}, d={d}) solve ({dts:.1f} s) by the C "
-                          "restatement of twedband.engine.twed_parallel (per-diagonal "
-                          f"parallel band), {threads} threads"),
-               "tuned_port": {"value": gct, "sample_n": nst,
-                              "what": "bit-identical tiled wavefront restatement (oracle "
-                                      "orc_band_tiled), same threads"},
+        kind = reference_kind()
+        gc, ns, dts = cpu_reference_rate(kind, d, wl["seed"], args.cpu_budget_s, threads)
+        cpu = {"value": gc, "unit": "GCUPS", "cores": threads, "kind": kind,
+               "sample": reference_sample_text(kind, ns, d, wl["seed"], threads, args.workload)
+               + f" ({dts:.1f} s)",
                "host": orc.host_description()}
+        if kind == "reference":
+            gp, np_, dtp = cpu_reference_rate("port", d, wl["seed"], args.cpu_budget_s / 2,
+                                              threads)
+            cpu["port"] = {"value": gp, "sample_n": np_,
+                           "what": "C restatement of the same band (oracle/), same threads"}
 
     if rank == 0:
         line = {
-            "metric": "TWED GCUPS (DP cells/s, n=1M pair)",
+            "metric": METRIC,
             "value": value, "unit": "GCUPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None,
