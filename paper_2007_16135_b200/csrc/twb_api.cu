@@ -90,12 +90,19 @@ void init_pool(int dev) {
 // negative-signed, the DP min is order-free and exact symmetry allows
 // swapping the pair. Otherwise the NaN-exact compare chain is used.
 // ---------------------------------------------------------------------------
+// tiny > 0 (fp32 values): nonzero |x| < tiny also counts as unsafe, because
+// the fp32 kernels take the square root with flush-to-zero (sqrt.approx.ftz)
+// on the safe path; with every nonzero |x| >= 2^-30 a nonzero sum of squared
+// differences is >= 2^-106, far above the fp32 denormal range.
 template <typename T>
-__global__ void unsafe_kernel(const T* __restrict__ x, int64_t n, double limit, int* flag) {
+__global__ void unsafe_kernel(const T* __restrict__ x, int64_t n, double limit, double tiny,
+                              int* flag) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     bool bad = false;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-        bad |= !(fabs((double)x[i]) < limit);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const double a = fabs((double)x[i]);
+        bad |= !(a < limit) || (a != 0.0 && a < tiny);
+    }
     if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
 }
 
@@ -126,10 +133,11 @@ __global__ void mirror_kernel(T* m, int64_t n) {
 }
 
 template <typename T>
-int check_unsafe(const T* d, int64_t n, double limit, int* dflag, cudaStream_t st) {
+int check_unsafe(const T* d, int64_t n, double limit, int* dflag, cudaStream_t st,
+                 double tiny = 0.0) {
     if (n <= 0) return 0;
     int blocks = (int)std::min<int64_t>((n + 255) / 256, 4096);
-    unsafe_kernel<T><<<blocks, 256, 0, st>>>(d, n, limit, dflag);
+    unsafe_kernel<T><<<blocks, 256, 0, st>>>(d, n, limit, tiny, dflag);
     ++t_launches;
     return 0;
 }
@@ -215,6 +223,10 @@ template <typename T>
 constexpr double safe_limit() {
     return sizeof(T) == 8 ? 0x1p500 : 0x1p60;
 }
+template <typename R>
+constexpr double safe_tiny() {
+    return sizeof(R) == 8 ? 0.0 : 0x1p-30;
+}
 
 // ---------------------------------------------------------------------------
 // Single pair. Inputs are device pointers (raw samples); out is a device
@@ -228,9 +240,9 @@ int twed_pair_dev(const T* dA, int64_t nA, const T* dTA, const T* dB, int64_t nB
     if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
     CK(cudaMemsetAsync(dflag, 0, sizeof(int), st));
     const double lim = safe_limit<R>();
-    check_unsafe(dA, nA * dim, lim, dflag, st);
+    check_unsafe(dA, nA * dim, lim, dflag, st, safe_tiny<R>());
     check_unsafe(dTA, nA, lim, dflag, st);
-    check_unsafe(dB, nB * dim, lim, dflag, st);
+    check_unsafe(dB, nB * dim, lim, dflag, st, safe_tiny<R>());
     check_unsafe(dTB, nB, lim, dflag, st);
     int hflag = 0;
     CK(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -363,10 +375,10 @@ int twed_batch_dev_impl(const T* dAA, const int64_t* a_off, int64_t nAA, const T
     }
     CK(cudaMemcpyAsync(d_bpoff, b_poff.data(), sizeof(int64_t) * (nBB + 1), cudaMemcpyHostToDevice, st));
     const double lim = safe_limit<R>();
-    check_unsafe(dAA, totA * dim, lim, dflag, st);
+    check_unsafe(dAA, totA * dim, lim, dflag, st, safe_tiny<R>());
     check_unsafe(dTAA, totA, lim, dflag, st);
     if (!self) {
-        check_unsafe(dBB, totB * dim, lim, dflag, st);
+        check_unsafe(dBB, totB * dim, lim, dflag, st, safe_tiny<R>());
         check_unsafe(dTBB, totB, lim, dflag, st);
     }
     int hflag = 0;
@@ -600,9 +612,58 @@ __global__ void add_probe_kernel(T* sink, int iters, T seed) {
     if (r == (T)-1) sink[0] = r;  // keep the chains alive
 }
 
+// sqrt_fast (twb_device.cuh) against __dsqrt_rn on hashed bit patterns: half
+// uniform over every non-negative double (all exponents, denormals, inf, NaN),
+// half uniform mantissas over exponents [2^-80, 2^80). Counts bit mismatches
+// where sqrt_fast_ok holds, and how many inputs took the fast path.
+__device__ __forceinline__ unsigned long long splitmix(unsigned long long x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+__global__ void sqrt_check_kernel(int64_t n, unsigned long long seed, unsigned long long* bad,
+                                  unsigned long long* fast) {
+    unsigned long long nb = 0, nf = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        unsigned long long h = splitmix(seed ^ (unsigned long long)i);
+        unsigned long long bits = h & 0x7fffffffffffffffull;
+        if (i & 1) {
+            const unsigned long long e = 0x3ff - 80 + ((h >> 52) % 160);
+            bits = (e << 52) | (h & 0x000fffffffffffffull);
+        }
+        const double x = __longlong_as_double((long long)bits);
+        if (sqrt_fast_ok(x)) {
+            ++nf;
+            nb += __double_as_longlong(sqrt_fast(x)) != __double_as_longlong(__dsqrt_rn(x));
+        }
+    }
+    atomicAdd(bad, nb);
+    atomicAdd(fast, nf);
+}
+
 }  // namespace
 
 extern "C" {
+
+int64_t twb_selftest_sqrt(int64_t n, uint64_t seed, int32_t device, int64_t* fast_count) {
+    if (n < 1) return fail(TWB_EINVAL, "n must be >= 1");
+    CK(cudaSetDevice(device));
+    cudaStream_t st = cudaStreamPerThread;
+    unsigned long long* d = nullptr;
+    CK(cudaMallocAsync(&d, 2 * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), st));
+    sqrt_check_kernel<<<148 * 8, 256, 0, st>>>(n, seed, d, d + 1);
+    ++t_launches;
+    CK(cudaGetLastError());
+    unsigned long long h[2] = {0, 0};
+    CK(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(d, st));
+    CK(cudaStreamSynchronize(st));
+    if (fast_count) *fast_count = (int64_t)h[1];
+    return (int64_t)h[0];
+}
 
 double twb_probe_add_rate(int fp64, int device) {
     if (cudaSetDevice(device) != cudaSuccess) return -1.0;

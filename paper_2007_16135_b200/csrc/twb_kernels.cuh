@@ -193,6 +193,7 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
         int sidx = 0, pos = 0;
         int curlen = slen[warp][0];
         Z zbot = INF;
+        R mbot = R(0);
         const int64_t nsteps = ncols + 31;
         for (int64_t s = 0; s < nsteps; ++s) {
             if ((s & 31) == 0) {
@@ -201,6 +202,8 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
                 stage_block<D>(ring, args.B, c0, ncols, (s >> 5) + 2, lane);
             }
             Z zup = __shfl_up_sync(FULL, zbot, 1);
+            R mup = R(0);
+            if constexpr (decltype(L)::SHUF_M) mup = __shfl_up_sync(FULL, mbot, 1);
             const int64_t j = s - lane;
             if (j >= 0 && j < ncols) {
                 const int slot = (int)(j & (RING_COLS - 1));
@@ -210,8 +213,11 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
                 const R tb = ring.t[slot];
                 const Z delb = ring.del[slot];
                 const bool col0 = pos == 0;
-                if (lane == 0) zup = col0 ? Z(0) : INF;  // row 0: z(0,0)=0, z(0,j)=inf
-                zbot = L.step(vb, tb, delb, zup, col0, args.nu, args.p);
+                if (lane == 0) {  // row 0: z(0,0)=0, z(0,j)=inf; d(0,j) only meets z=inf
+                    zup = col0 ? Z(0) : INF;
+                    mup = R(0);
+                }
+                zbot = L.step(vb, tb, delb, zup, mup, col0, args.nu, args.p, mbot);
                 if (++pos == curlen) {
                     if (lane == own_lane) {
                         const Z v = L.z_at(own_q);
@@ -241,9 +247,11 @@ template <int D, typename R, typename Z>
 __host__ __device__ constexpr size_t wave_smem_rings(int warps) {
     return (sizeof(ColRing<D, R, Z>) * warps + 15) / 16 * 16;
 }
+// rings | zring[W][ZRS] | mring[W][ZRS] | gstage z[64] | gstage m[64] | prog[W] | cons[W]
 template <int D, typename R, typename Z>
 __host__ __device__ constexpr size_t wave_smem(int warps) {
-    return wave_smem_rings<D, R, Z>(warps) + sizeof(Z) * (ZRS * warps + 64) + sizeof(int) * 2 * warps;
+    return wave_smem_rings<D, R, Z>(warps) + sizeof(Z) * (ZRS * warps + 64) +
+           sizeof(R) * (ZRS * warps + 64) + sizeof(int) * 2 * warps;
 }
 
 template <typename R, typename Z>
@@ -252,7 +260,8 @@ struct WaveArgs {
     int64_t nA, nB;
     int64_t S;  // stripes
     int64_t H;  // rows per stripe
-    Z* gbuf;            // gridDim.x x (nB+1): bottom row of the CTA's current stripe
+    Z* gbuf;            // gridDim.x x (nB+1): bottom row z of the CTA's current stripe
+    R* gmbuf;           // gridDim.x x (nB+1): bottom row d(r, j) (d >= 2)
     long long* gprog;   // gridDim.x progress counters: stripe*(nB+1) + columns published
     double nu;
     int p;
@@ -261,11 +270,20 @@ struct WaveArgs {
 
 template <int D, int K, int P, bool EXACT_NAN, bool NU1, int WARPS, typename R, typename Z>
 __global__ void __launch_bounds__(WARPS * 32, 1) wave_kernel(const WaveArgs<R, Z> args) {
+    using Lane = LaneRows<D, K, P, EXACT_NAN, NU1, R, Z>;
+    constexpr bool SHUF_M = Lane::SHUF_M;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto* rings = reinterpret_cast<ColRing<D, R, Z>*>(smem_raw);
-    auto* zring = reinterpret_cast<Z(*)[ZRS]>(smem_raw + wave_smem_rings<D, R, Z>(WARPS));
-    Z* gstage = reinterpret_cast<Z*>(smem_raw + wave_smem_rings<D, R, Z>(WARPS) + sizeof(Z) * ZRS * WARPS);
-    int* prog = reinterpret_cast<int*>(gstage + 64);
+    unsigned char* p0 = smem_raw + wave_smem_rings<D, R, Z>(WARPS);
+    auto* zring = reinterpret_cast<Z(*)[ZRS]>(p0);
+    p0 += sizeof(Z) * ZRS * WARPS;
+    auto* mring = reinterpret_cast<R(*)[ZRS]>(p0);
+    p0 += sizeof(R) * ZRS * WARPS;
+    Z* gstage = reinterpret_cast<Z*>(p0);
+    p0 += sizeof(Z) * 64;
+    R* gmstage = reinterpret_cast<R*>(p0);
+    p0 += sizeof(R) * 64;
+    int* prog = reinterpret_cast<int*>(p0);
     int* cons = prog + WARPS;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -275,7 +293,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) wave_kernel(const WaveArgs<R, Z
     ColRing<D, R, Z>& ring = rings[warp];
     const Z INF = zinf<Z>();
     const int64_t ncols = args.nB + 1;
-    LaneRows<D, K, P, EXACT_NAN, NU1, R, Z> L;
+    Lane L;
 
     const int64_t s_last = (args.nA - 1) / args.H;
     const int64_t loc_last = (args.nA - 1) - s_last * args.H;
@@ -308,8 +326,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) wave_kernel(const WaveArgs<R, Z
         const long long gbase_out = (long long)s * ncols;
         Z* grow_out = args.gbuf + (int64_t)b * ncols;
         const Z* grow_in = args.gbuf + (int64_t)pb * ncols;
+        R* gmrow_out = SHUF_M ? args.gmbuf + (int64_t)b * ncols : nullptr;
+        const R* gmrow_in = SHUF_M ? args.gmbuf + (int64_t)pb * ncols : nullptr;
 
         Z zbot = INF;
+        R mbot = R(0);
         const int64_t nsteps = ncols + 31;
         for (int64_t st = 0; st < nsteps; ++st) {
             if ((st & 31) == 0) {
@@ -321,7 +342,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) wave_kernel(const WaveArgs<R, Z
                     const long long need = gbase_in + min(st + CHG, ncols);
                     while (ld_acquire_gpu(args.gprog + pb) < need) __nanosleep(20);
                     const int64_t c = st + lane;
-                    if (c < ncols) gstage[c & 63] = __ldcg(grow_in + c);
+                    if (c < ncols) {
+                        gstage[c & 63] = __ldcg(grow_in + c);
+                        if constexpr (SHUF_M) gmstage[c & 63] = __ldcg(gmrow_in + c);
+                    }
                     __syncwarp();
                 }
             }
@@ -338,6 +362,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) wave_kernel(const WaveArgs<R, Z
                 }
             }
             Z zup = __shfl_up_sync(FULL, zbot, 1);
+            R mup = R(0);
+            if constexpr (SHUF_M) mup = __shfl_up_sync(FULL, mbot, 1);
             const int64_t j = st - lane;
             if (j >= 0 && j < ncols) {
                 const int slot = (int)(j & (RING_COLS - 1));
@@ -348,18 +374,27 @@ __global__ void __launch_bounds__(WARPS * 32, 1) wave_kernel(const WaveArgs<R, Z
                 const Z delb = ring.del[slot];
                 const bool col0 = j == 0;
                 if (lane == 0) {
-                    if (warp > 0) zup = zring[warp][j % ZRS];
-                    else if (top_boundary) zup = col0 ? Z(0) : INF;
-                    else zup = gstage[j & 63];
+                    if (warp > 0) {
+                        zup = zring[warp][j % ZRS];
+                        if constexpr (SHUF_M) mup = mring[warp][j % ZRS];
+                    } else if (top_boundary) {
+                        zup = col0 ? Z(0) : INF;  // row 0; d(0, j) only meets z = inf
+                        mup = R(0);
+                    } else {
+                        zup = gstage[j & 63];
+                        if constexpr (SHUF_M) mup = gmstage[j & 63];
+                    }
                 }
-                zbot = L.step(vb, tb, delb, zup, col0, args.nu, args.p);
+                zbot = L.step(vb, tb, delb, zup, mup, col0, args.nu, args.p, mbot);
                 if (lane == 31) {
                     if (to_ring) {
                         zring[warp + 1][j % ZRS] = zbot;
+                        if constexpr (SHUF_M) mring[warp + 1][j % ZRS] = mbot;
                         if (((j + 1) % CHS) == 0 || j == ncols - 1)
                             st_release_cta(&prog[warp + 1], (int)(j + 1));
                     } else if (to_global) {
                         grow_out[j] = zbot;
+                        if constexpr (SHUF_M) gmrow_out[j] = mbot;
                         if (((j + 1) % CHG) == 0 || j == ncols - 1)
                             st_release_gpu(args.gprog + b, gbase_out + j + 1);
                     }

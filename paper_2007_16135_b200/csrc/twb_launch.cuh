@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "twb_kernels.cuh"
 
@@ -97,11 +98,35 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * 32, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorLaunchOutOfResources;
-    const int64_t H = (int64_t)W * 32 * K;
-    const int64_t S = (pr.nA + H - 1) / H;
+    // Stripe height: ws active warps of 32*K rows (ws <= W). Every stripe
+    // sweeps all nB+1 columns, so a round of G co-resident stripes costs about
+    // nB steps however many rows it holds, and the pipeline fill adds
+    // ~(32 + CHS) steps per warp of the whole first round. Pick ws so the
+    // stripes fill every SM slot in the fewest rounds (e.g. n = 1M, K = 8:
+    // 7 warps -> 559 stripes = 3.8 rounds of 148, instead of 8 warps -> 489
+    // stripes on only 123 SMs).
     const int64_t cap = (int64_t)sms * occ;
-    const int64_t rounds = (S + cap - 1) / cap;
-    const int64_t G = (S + rounds - 1) / rounds;
+    int64_t H = 0, S = 0, G = 0;
+    double best = 0;
+    // TWB_WAVE_WS=<n> pins the active warps per stripe (tuning experiments).
+    int ws_pin = 0;
+    if (const char* env = getenv("TWB_WAVE_WS")) ws_pin = atoi(env);
+    for (int ws = W; ws >= 1; --ws) {
+        if (ws_pin > 0 && ws != (ws_pin < W ? ws_pin : W)) continue;
+        const int64_t h = (int64_t)ws * 32 * K;
+        const int64_t s = (pr.nA + h - 1) / h;
+        const int64_t r = (s + cap - 1) / cap;
+        const int64_t g = (s + r - 1) / r;
+        const double cost = (double)r * (double)(pr.nB + 32) +
+                            (double)g * (double)(ws * (32 + CHS) + CHG) +
+                            (double)(W - ws) * 1e-6;  // ties -> more warps
+        if (H == 0 || cost < best) {
+            best = cost;
+            H = h;
+            S = s;
+            G = g;
+        }
+    }
     WaveArgs<R, Z> a;
     a.A = pr.A;
     a.B = pr.B;
@@ -113,8 +138,10 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
     a.p = pr.p;
     a.out = pr.out;
     a.gbuf = (Z*)alloc.get(sizeof(Z) * (size_t)G * (size_t)(pr.nB + 1));
+    constexpr bool shuf = LaneRows<D, K, P, E, N1, R, Z>::SHUF_M;
+    a.gmbuf = shuf ? (R*)alloc.get(sizeof(R) * (size_t)G * (size_t)(pr.nB + 1)) : nullptr;
     a.gprog = (long long*)alloc.get(sizeof(long long) * (size_t)G);
-    if (!a.gbuf || !a.gprog) return cudaErrorMemoryAllocation;
+    if (!a.gbuf || !a.gprog || (shuf && !a.gmbuf)) return cudaErrorMemoryAllocation;
     e = cudaMemsetAsync(a.gprog, 0, sizeof(long long) * (size_t)G, st);
     if (e != cudaSuccess) return e;
     void* params[] = {(void*)&a};

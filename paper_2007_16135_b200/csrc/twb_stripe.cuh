@@ -117,19 +117,64 @@ __device__ __forceinline__ Z zinf() {
     else return __int_as_float(0x7f800000);
 }
 
+// Sum of squared differences, the p == 2 accumulator of lp_dist
+// (_kernels.py:39-44: acc = 0.0; acc += diff*diff, sequentially).
+template <int D>
+__device__ __forceinline__ double sumsq(const double (&x)[D], const double (&y)[D]) {
+    double d0 = x[0] - y[0];
+    double acc = __dmul_rn(d0, d0);
+#pragma unroll
+    for (int k = 1; k < D; ++k) {
+        double dk = x[k] - y[k];
+        acc = __dadd_rn(acc, __dmul_rn(dk, dk));
+    }
+    return acc;
+}
+
+// fp32 square root: sqrt.approx (MUFU.SQRT). FTZ on the proven-safe path
+// (the host flags nonzero |x| < 2^-30 as unsafe, so a nonzero sum of squares
+// is never denormal there); the exact-NaN path keeps denormal handling.
+template <bool FTZ>
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    if constexpr (FTZ) asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    else asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // Per-lane DP state for K rows.
+//
+// fp64 (bit-exact): per row the lane keeps d(r, j-1) and t_a(r) - t_b(j-1),
+// the d_prev and second t-gap term of interior_cost for (r+1, j), and sums in
+// the reference's association.
+// fp32 modes (tolerance 1e-5): per row it keeps the edge cost
+// c(r, j-1) = d(r, j-1) + nu*|t_a(r) - t_b(j-1)|, so the match candidate is
+// z_diag + (c(r, j) + c(r-1, j-1)) -- the same terms regrouped, 3 adds per cell
+// instead of 5, and sums of squares use FMA.
+//
+// SHUF_M: the d_prev (fp64) / c (fp32) of the lane's first row is the value
+// the lane above computed for its last row two steps earlier; it arrives by
+// shuffle (or through the warp/CTA boundary rings) instead of being
+// recomputed. Same value, same bits.
+// SPLIT_SQRT (fp64, d >= 2, degree 2): the K square roots of a step run as
+// straight-line sqrt_fast (interleavable), with one rare fix-up branch per
+// step for out-of-range arguments (twb_device.cuh).
 template <int D, int K, int P, bool EXACT_NAN, bool NU1, typename R, typename Z>
 struct LaneRows {
+    static constexpr bool F32 = sizeof(R) == 4;
+    static constexpr bool SHUF_M = D >= 2 || F32;
+    static constexpr bool SPLIT_SQRT = !F32 && D >= 2 && P == 2;
     R a[K][D];
     R ta[K];
     Z da[K];
     Z zl[K];  // z(r, j-1)
-    R mr[K];  // d(r, j-1)
-    R gr[K];  // t_a(r) - t_b(j-1) (signed, |.| at use)
+    R mr[K];  // fp64: d(r, j-1); fp32: c(r, j-1)
+    R gr[K];  // fp64: t_a(r) - t_b(j-1) (signed, |.| at use)
     Z zupp;   // z(r0-1, j-1)
+    R mupp;   // d(r0-1, j-1) / c(r0-1, j-1) (SHUF_M)
     R aup[D];
     R tup;
-    R vbp[D];  // column j-1 values (top-row recompute)
+    R vbp[D];  // column j-1 values (top-row recompute, !SHUF_M)
     R tbp;
 
     // Rows [r0, r0+K) of the prepared series at `base`; rows > n are zero
@@ -156,6 +201,7 @@ struct LaneRows {
         for (int k = 0; k < D; ++k) vbp[k] = R(0);
         tbp = R(0);
         zupp = zinf<Z>();
+        mupp = R(0);
 #pragma unroll
         for (int q = 0; q < K; ++q) {
             zl[q] = zinf<Z>();
@@ -164,55 +210,110 @@ struct LaneRows {
         }
     }
 
+    // d(r, j) for the lane's K rows.
+    __device__ __forceinline__ void dists(const R (&vb)[D], int p, R (&mn)[K]) const {
+        if constexpr (SPLIT_SQRT) {
+            bool ok = true;
+#pragma unroll
+            for (int q = 0; q < K; ++q) {
+                const double acc = sumsq<D>(a[q], vb);
+                ok &= sqrt_fast_ok(acc);
+                mn[q] = sqrt_fast(acc);
+            }
+            if (!ok) {
+#pragma unroll
+                for (int q = 0; q < K; ++q) {
+                    const double acc = sumsq<D>(a[q], vb);
+                    if (!sqrt_fast_ok(acc)) mn[q] = __dsqrt_rn(acc);
+                }
+            }
+        } else if constexpr (F32 && D >= 2 && P == 2) {
+#pragma unroll
+            for (int q = 0; q < K; ++q) {
+                const float d0 = a[q][0] - vb[0];
+                float acc = d0 * d0;
+#pragma unroll
+                for (int k = 1; k < D; ++k) {
+                    const float dk = a[q][k] - vb[k];
+                    acc = __fmaf_rn(dk, dk, acc);
+                }
+                mn[q] = sqrt_approx<!EXACT_NAN>(acc);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < K; ++q) mn[q] = dist<D, P, R>(a[q], vb, p);
+        }
+    }
+
     // One column j for the K rows (interior_cost, _kernels.py:61-80, per row).
-    // zup = z(r0-1, j). col0: j is a virtual column 0 (z(r, 0) = +inf, r >= 1).
-    // Returns z(r0+K-1, j).
-    __device__ __forceinline__ Z step(const R (&vb)[D], R tb, Z delb, Z zup, bool col0, double nu,
-                                      int p) {
-        // d(r0-1, j-1) and t_a(r0-1) - t_b(j-1): same inputs and operations as
-        // the lane above used one step earlier -> bit-identical recompute.
-        R m_up = dist<D, P, R>(aup, vbp, p);
-        R g_up = tup - tbp;
+    // zup = z(r0-1, j); mup = d(r0-1, j) / c(r0-1, j) (SHUF_M; used one step
+    // later). col0: j is a virtual column 0 (z(r, 0) = +inf, r >= 1).
+    // Returns z(r0+K-1, j); mbot = d / c of row r0+K-1 at j.
+    __device__ __forceinline__ Z step(const R (&vb)[D], R tb, Z delb, Z zup, R mup, bool col0,
+                                      double nu, int p, R& mbot) {
+        R mn[K];
+        dists(vb, p, mn);
+        const Z INF = zinf<Z>();
         Z zu = zup;
         Z zd = zupp;
-        const Z INF = zinf<Z>();
+        if constexpr (F32) {
+            const float nuf = (float)nu;
+            R c_up = mupp;
 #pragma unroll
-        for (int q = 0; q < K; ++q) {
-            const R m = dist<D, P, R>(a[q], vb, p);
-            const R g = ta[q] - tb;
-            Z match;
-            if constexpr (sizeof(R) == 8) {
+            for (int q = 0; q < K; ++q) {
+                const float g = ta[q] - tb;
+                const float c = NU1 ? mn[q] + fabsf(g) : __fmaf_rn(nuf, fabsf(g), mn[q]);
+                const float w = c + c_up;
+                Z match;
+                if constexpr (sizeof(Z) == 4) match = zd + w;
+                else match = zd + (double)w;  // fp32 local cost, fp64 accumulator
+                const Z del_b = zl[q] + delb;
+                const Z del_a = zu + da[q];
+                Z z = cell_min<EXACT_NAN>(del_a, del_b, match);
+                z = col0 ? INF : z;
+                zd = zl[q];
+                zl[q] = z;
+                zu = z;
+                c_up = mr[q];
+                mr[q] = c;
+            }
+        } else {
+            // d(r0-1, j-1) and t_a(r0-1) - t_b(j-1): the values the lane above
+            // computed two steps earlier (SHUF_M) or the same operations on
+            // the same inputs (bit-identical recompute).
+            R m_up;
+            if constexpr (SHUF_M) m_up = mupp;
+            else m_up = dist<D, P, R>(aup, vbp, p);
+            R g_up = tup - tbp;
+#pragma unroll
+            for (int q = 0; q < K; ++q) {
+                const R m = mn[q];
+                const R g = ta[q] - tb;
                 // ((z_diag + d_now) + d_prev) + nu * (|g_now| + |g_prev|)
                 const double gs = __dadd_rn(fabs(g), fabs(g_up));
                 const double tt = NU1 ? gs : __dmul_rn(nu, gs);
-                match = __dadd_rn(__dadd_rn(__dadd_rn(zd, m), m_up), tt);
-            } else if constexpr (sizeof(Z) == 4) {
-                const float gs = fabsf(g) + fabsf(g_up);
-                const float tt = NU1 ? gs : (float)nu * gs;
-                match = ((zd + m) + m_up) + tt;
-            } else {
-                // fp32 local cost, fp64 accumulator
-                const float gs = fabsf(g) + fabsf(g_up);
-                const float tt = NU1 ? gs : (float)nu * gs;
-                const float w = (m + m_up) + tt;
-                match = zd + (double)w;
+                const Z match = __dadd_rn(__dadd_rn(__dadd_rn(zd, m), m_up), tt);
+                const Z del_b = zl[q] + delb;
+                const Z del_a = zu + da[q];
+                Z z = cell_min<EXACT_NAN>(del_a, del_b, match);
+                z = col0 ? INF : z;
+                zd = zl[q];
+                zl[q] = z;
+                zu = z;
+                m_up = mr[q];
+                g_up = gr[q];
+                mr[q] = m;
+                gr[q] = g;
             }
-            const Z del_b = zl[q] + delb;
-            const Z del_a = zu + da[q];
-            Z z = cell_min<EXACT_NAN>(del_a, del_b, match);
-            z = col0 ? INF : z;
-            zd = zl[q];
-            zl[q] = z;
-            zu = z;
-            m_up = mr[q];
-            g_up = gr[q];
-            mr[q] = m;
-            gr[q] = g;
         }
         zupp = zup;
+        mupp = mup;
+        if constexpr (!SHUF_M) {
 #pragma unroll
-        for (int k = 0; k < D; ++k) vbp[k] = vb[k];
+            for (int k = 0; k < D; ++k) vbp[k] = vb[k];
+        }
         tbp = tb;
+        mbot = mr[K - 1];
         return zu;
     }
 

@@ -247,6 +247,36 @@ def test_device_resident_api(twb):
     assert out.item() == want
 
 
+def test_sqrt_split_bit_exact(twb):
+    """The DP kernels' straight-line fp64 sqrt equals __dsqrt_rn bit for bit."""
+    import ctypes
+    from paper_2007_16135_b200 import _lib
+    lib = _lib.load()
+    fast = ctypes.c_int64(0)
+    bad = lib.twb_selftest_sqrt(1 << 26, 20261017, 0, ctypes.byref(fast))
+    assert bad == 0, bad
+    assert fast.value > (1 << 24)
+
+
+@pytest.mark.parametrize("scale", [1e-170, 1e-150, 1.0, 1e150, 1e240])
+def test_extreme_magnitudes_vs_oracle(twb, oracle, scale):
+    """Tiny and huge values send sqrt arguments outside the fast path (zero,
+    denormal squares) or close to overflow; results stay bit-identical."""
+    rng = np.random.default_rng(int(abs(np.log10(scale))) + 7)
+    for d in (2, 3):
+        a = np.cumsum(rng.standard_normal((300, d)), axis=0) * scale
+        b = np.cumsum(rng.standard_normal((257, d)), axis=0) * scale
+        b[::17] = a[:len(b[::17])]  # exact matches -> zero distances
+        ta, tb = np.arange(300.0), np.arange(257.0)
+        for nu, lam in ((1.0, 1.0), (0.5, 0.0)):
+            got = twb.twed(a, ta, b, tb, nu=nu, lam=lam, degree=2)
+            want = oracle.twed(a, ta, b, tb, nu, lam, 2)
+            assert same_float(got, want), (scale, d, nu, lam, got, want)
+            R = twb.twed_batch([a, b, a[:100]], None, None, None, nu, lam, 2, True)
+            assert same_float(R[0, 1], want)
+            assert R[0, 0] == 0.0 and R[1, 1] == 0.0
+
+
 def test_validation_messages(twb):
     with pytest.raises(ValueError, match="3 timestamps for 2 samples"):
         twb.twed([[1.0], [2.0]], [0.0, 1.0, 2.0], [1.0], [0.0])
