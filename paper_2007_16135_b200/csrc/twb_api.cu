@@ -408,30 +408,35 @@ int twed_batch_dev_impl(const T* dAA, const int64_t* a_off, int64_t nAA, const T
     double avg_b = (double)totB / (double)nBB;
     int chunk = (int)std::lround(3072.0 / (avg_b + 1.0));
     chunk = std::max(1, std::min(chunk, MAX_CHUNK));
-    std::vector<int64_t> prefix(nrows + 1, 0);
+    // Rows longer than the warp kernel's reach go to the wavefront kernel; the
+    // others are grouped 32/LW consecutive rows per warp (row groups, see
+    // batch_kernel). A group's tasks cover the columns of its first row.
     std::vector<int64_t> long_rows;
     int64_t max_rows = 1;
     for (int64_t li = 0; li < nrows; ++li) {
-        const int64_t i = row_begin + li;
-        const int64_t na = a_off[i + 1] - a_off[i];
-        const int64_t jfirst = tri ? i : 0;
-        int64_t nt = 0;
-        if (na <= BATCH_ROWS_MAX) {
-            nt = nBB > jfirst ? (nBB - jfirst + chunk - 1) / chunk : 0;
-            max_rows = std::max(max_rows, na);
-        } else {
-            long_rows.push_back(li);
-        }
-        prefix[li + 1] = prefix[li] + nt;
+        const int64_t na = a_off[row_begin + li + 1] - a_off[row_begin + li];
+        if (na <= BATCH_ROWS_MAX) max_rows = std::max(max_rows, na);
+        else long_rows.push_back(li);
+    }
+    const int64_t groups_per_warp = 32 / batch_lanes(max_rows);
+    const int64_t ngroups = (nrows + groups_per_warp - 1) / groups_per_warp;
+    std::vector<int64_t> prefix(ngroups + 1, 0);
+    for (int64_t g = 0; g < ngroups; ++g) {
+        bool any_short = false;
+        for (int64_t li = g * groups_per_warp; li < std::min(nrows, (g + 1) * groups_per_warp); ++li)
+            any_short |= a_off[row_begin + li + 1] - a_off[row_begin + li] <= BATCH_ROWS_MAX;
+        const int64_t jfirst = tri ? row_begin + g * groups_per_warp : 0;
+        const int64_t nt = any_short && nBB > jfirst ? (nBB - jfirst + chunk - 1) / chunk : 0;
+        prefix[g + 1] = prefix[g] + nt;
     }
     CK(cudaStreamSynchronize(st));  // hflag (and the host vectors stay alive)
     const Variant v = pick_variant(dim, degree, nu, lam, hflag != 0, lim);
 
-    if (prefix[nrows] > 0) {
-        int64_t* d_prefix = sc.get_n<int64_t>(nrows + 1);
+    if (prefix[ngroups] > 0) {
+        int64_t* d_prefix = sc.get_n<int64_t>(ngroups + 1);
         unsigned long long* d_counter = sc.get_n<unsigned long long>(1);
         if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
-        CK(cudaMemcpyAsync(d_prefix, prefix.data(), sizeof(int64_t) * (nrows + 1),
+        CK(cudaMemcpyAsync(d_prefix, prefix.data(), sizeof(int64_t) * (ngroups + 1),
                            cudaMemcpyHostToDevice, st));
         CK(cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), st));
         BatchArgs<R, Z> a;
@@ -443,7 +448,8 @@ int twed_batch_dev_impl(const T* dAA, const int64_t* a_off, int64_t nAA, const T
         a.row_begin = row_begin;
         a.nrows = nrows;
         a.task_prefix = d_prefix;
-        a.ntasks = prefix[nrows];
+        a.ngroups = ngroups;
+        a.ntasks = prefix[ngroups];
         a.chunk = chunk;
         a.tri = tri;
         a.mirror = mirror;

@@ -59,7 +59,10 @@ __global__ void prepare_kernel(const T* __restrict__ values, const T* __restrict
         if (i >= ntot) {  // virtual row of series k
             int64_t k = i - ntot;
             int64_t o = (uniform_n > 0 ? k * uniform_n : off[k]) + k;
-            for (int c = 0; c < d; ++c) V[o * d + c] = R(0);
+            // fp32 batch layout (R = Z = float): +inf values mark the virtual
+            // column for LaneRows::COL0_BY_INF; otherwise the zero vector.
+            const R v0 = (sizeof(R) == 4 && sizeof(Z) == 4) ? (R)dinf() : R(0);
+            for (int c = 0; c < d; ++c) V[o * d + c] = v0;
             Tm[o] = R(0);
             Del[o] = (Z)dinf();
             continue;
@@ -135,7 +138,8 @@ struct BatchArgs {
     int64_t nBB;
     int64_t row_begin;           // first A series of this shard
     int64_t nrows;               // A series in this shard
-    const int64_t* task_prefix;  // (nrows+1) tasks before local row
+    const int64_t* task_prefix;  // (ngroups+1) tasks before local row group
+    int64_t ngroups;             // row groups of 32/LW consecutive local rows
     int64_t ntasks;
     int chunk;   // B series per task (<= MAX_CHUNK)
     int tri;     // only j >= i (engine.py:200-201)
@@ -147,81 +151,105 @@ struct BatchArgs {
     unsigned long long* counter;
 };
 
-template <int D, int K, int P, bool EXACT_NAN, bool NU1, int WARPS, typename R, typename Z>
+// Lanes per A series: 16 when every row-side series has <= 128 samples (two
+// series per warp share one staged B stream), else 32.
+__host__ __device__ constexpr int batch_lanes(int64_t max_rows) { return max_rows <= 128 ? 16 : 32; }
+
+// One warp per task = (row group, run of `chunk` B series). A row group is
+// 32/LW consecutive A series (LW lanes each, K rows per lane, rows in
+// registers); all of them stream the same B series back to back through one
+// cp.async-staged shared-memory ring, each B series with its virtual column 0,
+// so the (LW-1)-step lane skew is paid once per task, not once per pair.
+template <int D, int K, int LW, int P, bool EXACT_NAN, bool NU1, int WARPS, typename R, typename Z>
 __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z> args) {
+    using Lane = LaneRows<D, K, P, EXACT_NAN, NU1, R, Z>;
+    constexpr int GROUPS = 32 / LW;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto* rings = reinterpret_cast<ColRing<D, R, Z>*>(smem_raw);
     auto* slen = reinterpret_cast<int(*)[MAX_CHUNK]>(smem_raw + sizeof(ColRing<D, R, Z>) * WARPS);
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const int grp = lane / LW;
+    const int hl = lane % LW;  // lane within the series' lane group
     ColRing<D, R, Z>& ring = rings[warp];
     const Z INF = zinf<Z>();
-    LaneRows<D, K, P, EXACT_NAN, NU1, R, Z> L;
+    Lane L;
 
     while (true) {
         unsigned long long task = 0;
         if (lane == 0) task = atomicAdd(args.counter, 1ull);
         task = __shfl_sync(FULL, task, 0);
         if ((int64_t)task >= args.ntasks) return;
-        // local row: last li with task_prefix[li] <= task
-        int64_t lo = 0, hi = args.nrows;
+        // row group: last gi with task_prefix[gi] <= task
+        int64_t lo = 0, hi = args.ngroups;
         while (hi - lo > 1) {
             int64_t mid = (lo + hi) >> 1;
             if (args.task_prefix[mid] <= (int64_t)task) lo = mid; else hi = mid;
         }
-        const int64_t li = lo;
-        const int64_t i = args.row_begin + li;
-        const int64_t jfirst = args.tri ? i : 0;
-        const int64_t j0 = jfirst + ((int64_t)task - args.task_prefix[li]) * args.chunk;
+        const int64_t li0 = lo * GROUPS;             // first local row of the group
+        const int64_t i0 = args.row_begin + li0;
+        const int64_t jfirst = args.tri ? i0 : 0;
+        const int64_t j0 = jfirst + ((int64_t)task - args.task_prefix[lo]) * args.chunk;
         const int64_t j1 = min(j0 + (int64_t)args.chunk, args.nBB);
         const int nser = (int)(j1 - j0);
 
+        const int64_t li = li0 + grp;  // this lane group's local row
+        const bool row_ok = li < args.nrows;
+        const int64_t i = args.row_begin + (row_ok ? li : li0);
         const int64_t abase = args.a_poff[i];
         const int64_t nA = args.a_poff[i + 1] - abase - 1;
-        L.load(args.A, abase, 1 + (int64_t)lane * K, nA);
+        L.load(args.A, abase, 1 + (int64_t)hl * K, nA);
         for (int k = lane; k < nser; k += 32)
             slen[warp][k] = (int)(args.b_poff[j0 + k + 1] - args.b_poff[j0 + k]);
         const int64_t c0 = args.b_poff[j0];
-        const int64_t ncols = args.b_poff[j1] - c0;
+        const int ncols = (int)(args.b_poff[j1] - c0);
         stage_block<D>(ring, args.B, c0, ncols, 0, lane);
         stage_block<D>(ring, args.B, c0, ncols, 1, lane);
         __syncwarp();
 
         const int own_lane = (int)((nA - 1) / K);
         const int own_q = (int)((nA - 1) % K);
+        const bool writer = row_ok && hl == own_lane;
         Z* orow = args.out + li * args.ld;
         int sidx = 0, pos = 0;
         int curlen = slen[warp][0];
         Z zbot = INF;
         R mbot = R(0);
-        const int64_t nsteps = ncols + 31;
-        for (int64_t s = 0; s < nsteps; ++s) {
+        const int nsteps = ncols + LW - 1;
+        for (int s = 0; s < nsteps; ++s) {
             if ((s & 31) == 0) {
                 cp_async_wait<1>();
                 __syncwarp();
                 stage_block<D>(ring, args.B, c0, ncols, (s >> 5) + 2, lane);
             }
-            Z zup = __shfl_up_sync(FULL, zbot, 1);
+            Z zup = __shfl_up_sync(FULL, zbot, 1, LW);
             R mup = R(0);
-            if constexpr (decltype(L)::SHUF_M) mup = __shfl_up_sync(FULL, mbot, 1);
-            const int64_t j = s - lane;
+            if constexpr (Lane::SHUF_M) mup = __shfl_up_sync(FULL, mbot, 1, LW);
+            const int j = s - hl;
             if (j >= 0 && j < ncols) {
-                const int slot = (int)(j & (RING_COLS - 1));
+                const int slot = j & (RING_COLS - 1);
                 R vb[D];
 #pragma unroll
                 for (int k = 0; k < D; ++k) vb[k] = ring.v[slot * D + k];
                 const R tb = ring.t[slot];
                 const Z delb = ring.del[slot];
                 const bool col0 = pos == 0;
-                if (lane == 0) {  // row 0: z(0,0)=0, z(0,j)=inf; d(0,j) only meets z=inf
-                    zup = col0 ? Z(0) : INF;
+                Z zpn = zup;
+                if (hl == 0) {  // row 0: z(0,0)=0, z(0,j)=inf; d(0,j) only meets z=inf
+                    if constexpr (Lane::COL0_BY_INF) {
+                        zup = INF;
+                        zpn = col0 ? Z(0) : INF;
+                    } else {
+                        zup = col0 ? Z(0) : INF;
+                        zpn = zup;
+                    }
                     mup = R(0);
                 }
-                zbot = L.step(vb, tb, delb, zup, mup, col0, args.nu, args.p, mbot);
+                zbot = L.step(vb, tb, delb, zup, mup, col0, args.nu, args.p, mbot, zpn);
                 if (++pos == curlen) {
-                    if (lane == own_lane) {
+                    const int64_t jj = j0 + sidx;
+                    if (writer && (!args.tri || jj >= i)) {
                         const Z v = L.z_at(own_q);
-                        const int64_t jj = j0 + sidx;
                         orow[jj] = v;
                         if (args.mirror && jj != i) args.out[(jj - args.row_begin) * args.ld + i] = v;
                     }
@@ -268,8 +296,8 @@ struct WaveArgs {
     double* out;
 };
 
-template <int D, int K, int P, bool EXACT_NAN, bool NU1, int WARPS, typename R, typename Z>
-__global__ void __launch_bounds__(WARPS * 32, 1) wave_kernel(const WaveArgs<R, Z> args) {
+template <int D, int K, int P, bool EXACT_NAN, bool NU1, int WARPS, int MINB, typename R, typename Z>
+__global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R, Z> args) {
     using Lane = LaneRows<D, K, P, EXACT_NAN, NU1, R, Z>;
     constexpr bool SHUF_M = Lane::SHUF_M;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -385,7 +413,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) wave_kernel(const WaveArgs<R, Z
                         if constexpr (SHUF_M) mup = gmstage[j & 63];
                     }
                 }
-                zbot = L.step(vb, tb, delb, zup, mup, col0, args.nu, args.p, mbot);
+                zbot = L.step(vb, tb, delb, zup, mup, col0, args.nu, args.p, mbot, zup);
                 if (lane == 31) {
                     if (to_ring) {
                         zring[warp + 1][j % ZRS] = zbot;

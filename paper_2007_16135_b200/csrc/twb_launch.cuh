@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <string>
 
 #include "twb_kernels.cuh"
 
@@ -47,9 +48,10 @@ struct WaveProblem {
     Z* out;  // device, one value
 };
 
-// Batch kernel variants: rows per lane K in {2, 4, 8} (series of up to 256
-// samples on the row side), 8 warps per CTA, persistent grid with an atomic
-// task counter.
+// Batch kernel variants (lanes per series LW, rows per lane K): row-side
+// series of <= 32 / 64 / 128 samples -> LW = 16, K = 2 / 4 / 8 (two series
+// per warp); <= 256 -> LW = 32, K = 8. 4 warps per CTA, persistent grid with an
+// atomic task counter. The host groups rows by batch_lanes(max_rows).
 constexpr int BATCH_WARPS = 4;
 constexpr int BATCH_KMAX = 8;
 
@@ -75,19 +77,20 @@ cudaError_t run_batch(BatchArgs<R, Z> a, int64_t max_rows, cudaStream_t st, Laun
         ctx->after(st);
         return cudaGetLastError();
     };
-    if (max_rows <= 32 * 2) return go(batch_kernel<D, 2, P, E, N1, BATCH_WARPS, R, Z>);
-    if (max_rows <= 32 * 4) return go(batch_kernel<D, 4, P, E, N1, BATCH_WARPS, R, Z>);
-    if (max_rows <= 32 * 8) return go(batch_kernel<D, 8, P, E, N1, BATCH_WARPS, R, Z>);
+    if (max_rows <= 16 * 2) return go(batch_kernel<D, 2, 16, P, E, N1, BATCH_WARPS, R, Z>);
+    if (max_rows <= 16 * 4) return go(batch_kernel<D, 4, 16, P, E, N1, BATCH_WARPS, R, Z>);
+    if (max_rows <= 16 * 8) return go(batch_kernel<D, 8, 16, P, E, N1, BATCH_WARPS, R, Z>);
+    if (max_rows <= 32 * 8) return go(batch_kernel<D, 8, 32, P, E, N1, BATCH_WARPS, R, Z>);
     return cudaErrorInvalidValue;
 }
 
 // Wavefront variants: (warps, k) in {(8, 2), (8, 8)} -- picked so that the
 // row stripes cover every SM (short pairs) or amortise the per-row top-row
 // recompute (long pairs).
-template <int D, int K, int P, bool E, bool N1, int W, typename R, typename Z>
+template <int D, int K, int P, bool E, bool N1, int W, int MINB, typename R, typename Z>
 cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream_t st,
                          LaunchCtx* ctx) {
-    auto kern = wave_kernel<D, K, P, E, N1, W, R, Z>;
+    auto kern = wave_kernel<D, K, P, E, N1, W, MINB, R, Z>;
     int sms = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -158,11 +161,23 @@ cudaError_t run_wave(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream
     int sms = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // TWB_WAVE_CFG pins a variant (tuning experiments, fp64 d = 3 only):
+    // k8w8 | k4w8x2 (two CTAs per SM) | k4w16 | k2w8 | k8w4x2
+    if constexpr (D == 3 && sizeof(R) == 8 && !E) {
+        if (const char* env = getenv("TWB_WAVE_CFG")) {
+            const std::string c(env);
+            if (c == "k8w8") return run_wave_cfg<D, 8, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k4w8x2") return run_wave_cfg<D, 4, P, E, N1, 8, 2, R, Z>(pr, alloc, st, ctx);
+            if (c == "k4w16") return run_wave_cfg<D, 4, P, E, N1, 16, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k2w8") return run_wave_cfg<D, 2, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k8w4x2") return run_wave_cfg<D, 8, P, E, N1, 4, 2, R, Z>(pr, alloc, st, ctx);
+        }
+    }
     // Long row side: 8 rows per lane (2048-row stripes). Otherwise 2 rows per
     // lane so that the stripes still spread over the SMs.
     if (pr.nA >= (int64_t)sms * 8 * 32 * 8 * 2)
-        return run_wave_cfg<D, 8, P, E, N1, 8, R, Z>(pr, alloc, st, ctx);
-    return run_wave_cfg<D, 2, P, E, N1, 8, R, Z>(pr, alloc, st, ctx);
+        return run_wave_cfg<D, 8, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
+    return run_wave_cfg<D, 2, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
 }
 
 }  // namespace twb

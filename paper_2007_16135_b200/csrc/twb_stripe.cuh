@@ -249,8 +249,15 @@ struct LaneRows {
     // zup = z(r0-1, j); mup = d(r0-1, j) / c(r0-1, j) (SHUF_M; used one step
     // later). col0: j is a virtual column 0 (z(r, 0) = +inf, r >= 1).
     // Returns z(r0+K-1, j); mbot = d / c of row r0+K-1 at j.
+    //
+    // COL0_BY_INF (fp32 batch, proven-safe inputs): the prepared virtual row 0
+    // of every series holds +inf values (prepare_kernel), so at a virtual
+    // column all three candidates are already +inf and no per-cell select is
+    // needed; the caller feeds zup = +inf above row 1 and zupp_next = 0 after
+    // the virtual column (z(0, 0) = 0 is the diagonal of cell (1, 1)).
+    static constexpr bool COL0_BY_INF = F32 && sizeof(Z) == 4 && !EXACT_NAN;
     __device__ __forceinline__ Z step(const R (&vb)[D], R tb, Z delb, Z zup, R mup, bool col0,
-                                      double nu, int p, R& mbot) {
+                                      double nu, int p, R& mbot, Z zupp_next) {
         R mn[K];
         dists(vb, p, mn);
         const Z INF = zinf<Z>();
@@ -270,7 +277,7 @@ struct LaneRows {
                 const Z del_b = zl[q] + delb;
                 const Z del_a = zu + da[q];
                 Z z = cell_min<EXACT_NAN>(del_a, del_b, match);
-                z = col0 ? INF : z;
+                if constexpr (!COL0_BY_INF) z = col0 ? INF : z;
                 zd = zl[q];
                 zl[q] = z;
                 zu = z;
@@ -306,7 +313,7 @@ struct LaneRows {
                 gr[q] = g;
             }
         }
-        zupp = zup;
+        zupp = zupp_next;
         mupp = mup;
         if constexpr (!SHUF_M) {
 #pragma unroll
