@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
 // ---------------------------------------------------------------------------
 constexpr int ZRS = 256;  // shared-memory ring between consecutive warps (columns)
 constexpr int CHS = 16;   // warp-to-warp publish granularity (columns)
-constexpr int CHG = 32;   // CTA-to-CTA publish granularity (columns)
+constexpr int CHG = 32;   // CTA-to-CTA read granularity (columns; publish = args.chg)
 
 template <int D, typename R, typename Z>
 __host__ __device__ constexpr size_t wave_smem_rings(int warps) {
@@ -291,6 +291,7 @@ struct WaveArgs {
     Z* gbuf;            // gridDim.x x (nB+1): bottom row z of the CTA's current stripe
     R* gmbuf;           // gridDim.x x (nB+1): bottom row d(r, j) (d >= 2)
     long long* gprog;   // gridDim.x progress counters: stripe*(nB+1) + columns published
+    int chg;            // publish granularity of the bottom row (power of 2, >= 32)
     double nu;
     int p;
     double* out;
@@ -357,6 +358,24 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         R* gmrow_out = SHUF_M ? args.gmbuf + (int64_t)b * ncols : nullptr;
         const R* gmrow_in = SHUF_M ? args.gmbuf + (int64_t)pb * ncols : nullptr;
 
+        // Previous stripe's bottom row (warp 0 of a non-top stripe): block k =
+        // columns [32k, 32k+32) is loaded into registers one block ahead
+        // (latency hidden behind 32 steps) and parked in the 64-entry gstage
+        // ring when block k starts.
+        const bool from_global = warp == 0 && !top_boundary;
+        Z pz = Z(0);
+        R pm = R(0);
+        auto fetch = [&](int64_t c0) {  // block starting at column c0 -> registers
+            const long long need = gbase_in + min(c0 + CHG, ncols);
+            while (ld_acquire_gpu(args.gprog + pb) < need) __nanosleep(32);
+            const int64_t c = c0 + lane;
+            if (c < ncols) {
+                pz = __ldcg(grow_in + c);
+                if constexpr (SHUF_M) pm = __ldcg(gmrow_in + c);
+            }
+        };
+        if (from_global) fetch(0);
+
         Z zbot = INF;
         R mbot = R(0);
         const int64_t nsteps = ncols + 31;
@@ -365,15 +384,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                 cp_async_wait<1>();
                 __syncwarp();
                 stage_block<D>(ring, args.B, 0, ncols, (st >> 5) + 2, lane);
-                if (warp == 0 && !top_boundary && st < ncols) {
-                    // previous stripe's bottom row, columns [st, st+32)
-                    const long long need = gbase_in + min(st + CHG, ncols);
-                    while (ld_acquire_gpu(args.gprog + pb) < need) __nanosleep(20);
+                if (from_global && st < ncols) {
                     const int64_t c = st + lane;
                     if (c < ncols) {
-                        gstage[c & 63] = __ldcg(grow_in + c);
-                        if constexpr (SHUF_M) gmstage[c & 63] = __ldcg(gmrow_in + c);
+                        gstage[c & 63] = pz;
+                        if constexpr (SHUF_M) gmstage[c & 63] = pm;
                     }
+                    if (st + 32 < ncols) fetch(st + 32);
                     __syncwarp();
                 }
             }
@@ -423,7 +440,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                     } else if (to_global) {
                         grow_out[j] = zbot;
                         if constexpr (SHUF_M) gmrow_out[j] = mbot;
-                        if (((j + 1) % CHG) == 0 || j == ncols - 1)
+                        if (((j + 1) & (args.chg - 1)) == 0 || j == ncols - 1)
                             st_release_gpu(args.gprog + b, gbase_out + j + 1);
                     }
                 }

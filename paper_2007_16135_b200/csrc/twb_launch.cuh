@@ -137,6 +137,14 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
     a.nB = pr.nB;
     a.S = S;
     a.H = H;
+    // Bottom-row publish granularity: every st.release.gpu costs the
+    // producing warp a GPU-scope fence, so publish every chg columns (more for
+    // long rows; the consumer lags far behind anyway). TWB_WAVE_CHG overrides.
+    int chg = 32;
+    while (chg < 256 && (int64_t)chg * 2048 <= pr.nB) chg *= 2;
+    if (const char* env = getenv("TWB_WAVE_CHG")) chg = atoi(env);
+    if (chg < 32 || (chg & (chg - 1))) chg = 32;
+    a.chg = chg;
     a.nu = pr.nu;
     a.p = pr.p;
     a.out = pr.out;
