@@ -142,15 +142,17 @@ int check_unsafe(const T* d, int64_t n, double limit, int* dflag, cudaStream_t s
     return 0;
 }
 
+// virt: value of the virtual row 0 of V -- 0 (the reference's layout) or
+// +inf (the DP kernels' marker of a virtual column, LaneRows::COL0_BY_INF).
 template <typename T, typename R, typename Z>
 int prepare(const T* values, const T* times, const int64_t* d_off, int64_t nseries, int64_t ntot,
             int64_t uniform_n, int dim, double nu, double lam, int degree, R* V, R* Tm, Z* Del,
-            cudaStream_t st) {
+            cudaStream_t st, double virt = HUGE_VAL) {
     const int64_t work = ntot + nseries;
     int blocks = (int)std::min<int64_t>((work + 255) / 256, 148 * 16);
     if (blocks < 1) blocks = 1;
     prepare_kernel<T, R, Z><<<blocks, 256, 0, st>>>(values, times, d_off, nseries, ntot, uniform_n,
-                                                    dim, nu, lam, degree, V, Tm, Del);
+                                                    dim, nu, lam, degree, virt, V, Tm, Del);
     ++t_launches;
     CK(cudaGetLastError());
     return 0;
@@ -835,6 +837,10 @@ int twb_band_solve_f64(const double* va, const double* ta, const double* dela, i
         const bool is_del = k == 2 || k == 5;  // del[0] = +inf by construction
         check_unsafe(d[k] + (is_del ? 1 : 0), n[k] - (is_del ? 1 : 0), lim, dflag, st);
     }
+    // the DP kernels' copy marks the virtual row 0 with +inf (COL0_BY_INF)
+    static const double infs[4] = {HUGE_VAL, HUGE_VAL, HUGE_VAL, HUGE_VAL};
+    CK(cudaMemcpyAsync(d[0], infs, sizeof(double) * dim, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d[3], infs, sizeof(double) * dim, cudaMemcpyHostToDevice, st));
     int hflag = 0;
     CK(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -875,7 +881,7 @@ int twb_prepare_series_f64(const double* values, const double* times, int64_t n,
     CK(cudaMemcpyAsync(dv, values, sizeof(double) * n * dim, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(dt, times, sizeof(double) * n, cudaMemcpyHostToDevice, st));
     int rc = prepare<double, double, double>(dv, dt, nullptr, 1, n, n, dim, nu, lam, degree, V, Tm,
-                                             Del, st);
+                                             Del, st, 0.0);
     if (rc) return rc;
     CK(cudaMemcpyAsync(ext_values, V, sizeof(double) * (n + 1) * dim, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(ext_times, Tm, sizeof(double) * (n + 1), cudaMemcpyDeviceToHost, st));

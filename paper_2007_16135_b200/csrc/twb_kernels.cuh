@@ -52,17 +52,17 @@ template <typename T, typename R, typename Z>
 __global__ void prepare_kernel(const T* __restrict__ values, const T* __restrict__ times,
                                const int64_t* __restrict__ off, int64_t nseries, int64_t ntot,
                                int64_t uniform_n, int d, double nu, double lam, int p,
-                               R* __restrict__ V, R* __restrict__ Tm, Z* __restrict__ Del) {
+                               double virt, R* __restrict__ V, R* __restrict__ Tm,
+                               Z* __restrict__ Del) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntot + nseries;
          i += stride) {
         if (i >= ntot) {  // virtual row of series k
             int64_t k = i - ntot;
             int64_t o = (uniform_n > 0 ? k * uniform_n : off[k]) + k;
-            // fp32 batch layout (R = Z = float): +inf values mark the virtual
-            // column for LaneRows::COL0_BY_INF; otherwise the zero vector.
-            const R v0 = (sizeof(R) == 4 && sizeof(Z) == 4) ? (R)dinf() : R(0);
-            for (int c = 0; c < d; ++c) V[o * d + c] = v0;
+            // virt: 0 (the reference's zero vector) or +inf (DP kernels'
+            // copy: marks the virtual column, LaneRows::COL0_BY_INF).
+            for (int c = 0; c < d; ++c) V[o * d + c] = (R)virt;
             Tm[o] = R(0);
             Del[o] = (Z)dinf();
             continue;
@@ -223,8 +223,7 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
                 stage_block<D>(ring, args.B, c0, ncols, (s >> 5) + 2, lane);
             }
             Z zup = __shfl_up_sync(FULL, zbot, 1, LW);
-            R mup = R(0);
-            if constexpr (Lane::SHUF_M) mup = __shfl_up_sync(FULL, mbot, 1, LW);
+            R mup = __shfl_up_sync(FULL, mbot, 1, LW);
             const int j = s - hl;
             if (j >= 0 && j < ncols) {
                 const int slot = j & (RING_COLS - 1);
@@ -300,7 +299,6 @@ struct WaveArgs {
 template <int D, int K, int P, bool EXACT_NAN, bool NU1, int WARPS, int MINB, typename R, typename Z>
 __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R, Z> args) {
     using Lane = LaneRows<D, K, P, EXACT_NAN, NU1, R, Z>;
-    constexpr bool SHUF_M = Lane::SHUF_M;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto* rings = reinterpret_cast<ColRing<D, R, Z>*>(smem_raw);
     unsigned char* p0 = smem_raw + wave_smem_rings<D, R, Z>(WARPS);
@@ -355,8 +353,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         const long long gbase_out = (long long)s * ncols;
         Z* grow_out = args.gbuf + (int64_t)b * ncols;
         const Z* grow_in = args.gbuf + (int64_t)pb * ncols;
-        R* gmrow_out = SHUF_M ? args.gmbuf + (int64_t)b * ncols : nullptr;
-        const R* gmrow_in = SHUF_M ? args.gmbuf + (int64_t)pb * ncols : nullptr;
+        R* gmrow_out = args.gmbuf + (int64_t)b * ncols;
+        const R* gmrow_in = args.gmbuf + (int64_t)pb * ncols;
 
         // Previous stripe's bottom row (warp 0 of a non-top stripe): block k =
         // columns [32k, 32k+32) is loaded into registers one block ahead
@@ -371,24 +369,25 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             const int64_t c = c0 + lane;
             if (c < ncols) {
                 pz = __ldcg(grow_in + c);
-                if constexpr (SHUF_M) pm = __ldcg(gmrow_in + c);
+                pm = __ldcg(gmrow_in + c);
             }
         };
         if (from_global) fetch(0);
 
-        Z zbot = INF;
-        R mbot = R(0);
-        const int64_t nsteps = ncols + 31;
-        for (int64_t st = 0; st < nsteps; ++st) {
+        // Warp-uniform per-step bookkeeping: column staging, boundary-row
+        // fetch, ring flow control with the neighbouring warps.
+        auto preamble = [&](int64_t st) {
             if ((st & 31) == 0) {
-                cp_async_wait<1>();
+                // wait for every staged block: the software-pipelined loop
+                // reads one column ahead, into the block staged 32 steps ago
+                cp_async_wait<0>();
                 __syncwarp();
                 stage_block<D>(ring, args.B, 0, ncols, (st >> 5) + 2, lane);
                 if (from_global && st < ncols) {
                     const int64_t c = st + lane;
                     if (c < ncols) {
                         gstage[c & 63] = pz;
-                        if constexpr (SHUF_M) gmstage[c & 63] = pm;
+                        gmstage[c & 63] = pm;
                     }
                     if (st + 32 < ncols) fetch(st + 32);
                     __syncwarp();
@@ -406,47 +405,115 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                 while (ld_acquire_cta(&cons[warp + 1]) < need) {
                 }
             }
-            Z zup = __shfl_up_sync(FULL, zbot, 1);
-            R mup = R(0);
-            if constexpr (SHUF_M) mup = __shfl_up_sync(FULL, mbot, 1);
-            const int64_t j = st - lane;
-            if (j >= 0 && j < ncols) {
-                const int slot = (int)(j & (RING_COLS - 1));
-                R vb[D];
-#pragma unroll
-                for (int k = 0; k < D; ++k) vb[k] = ring.v[slot * D + k];
-                const R tb = ring.t[slot];
-                const Z delb = ring.del[slot];
-                const bool col0 = j == 0;
-                if (lane == 0) {
-                    if (warp > 0) {
-                        zup = zring[warp][j % ZRS];
-                        if constexpr (SHUF_M) mup = mring[warp][j % ZRS];
-                    } else if (top_boundary) {
-                        zup = col0 ? Z(0) : INF;  // row 0; d(0, j) only meets z = inf
-                        mup = R(0);
-                    } else {
-                        zup = gstage[j & 63];
-                        if constexpr (SHUF_M) mup = gmstage[j & 63];
-                    }
+        };
+        // The row above lane 0 at column st (lane 0's column), read by every
+        // lane from a warp-uniform address, selected for lane 0.
+        auto top_input = [&](int64_t st, Z& zup, R& mup, Z& zpn) {
+            Z zt;
+            R mt;
+            Z pn;
+            if (warp > 0) {
+                zt = zring[warp][st % ZRS];
+                mt = mring[warp][st % ZRS];
+                pn = zt;
+            } else if (top_boundary) {  // row 0; d(0, j) only meets z = inf
+                const bool c0 = st == 0;
+                if constexpr (Lane::COL0_BY_INF) {
+                    zt = INF;
+                    pn = c0 ? Z(0) : INF;
+                } else {
+                    zt = c0 ? Z(0) : INF;
+                    pn = zt;
                 }
-                zbot = L.step(vb, tb, delb, zup, mup, col0, args.nu, args.p, mbot, zup);
+                mt = R(0);
+            } else {
+                zt = gstage[st & 63];
+                mt = gmstage[st & 63];
+                pn = zt;
+            }
+            if (lane == 0) {
+                zup = zt;
+                mup = mt;
+                zpn = pn;
+            }
+        };
+        // Lane 31's bottom row at column st - 31 -> next warp / next stripe.
+        auto bottom_output = [&](int64_t st, Z zbot, R mbot) {
+            const int64_t j = st - 31;
+            if (to_ring) {
                 if (lane == 31) {
-                    if (to_ring) {
-                        zring[warp + 1][j % ZRS] = zbot;
-                        if constexpr (SHUF_M) mring[warp + 1][j % ZRS] = mbot;
-                        if (((j + 1) % CHS) == 0 || j == ncols - 1)
-                            st_release_cta(&prog[warp + 1], (int)(j + 1));
-                    } else if (to_global) {
-                        grow_out[j] = zbot;
-                        if constexpr (SHUF_M) gmrow_out[j] = mbot;
-                        if (((j + 1) & (args.chg - 1)) == 0 || j == ncols - 1)
-                            st_release_gpu(args.gprog + b, gbase_out + j + 1);
-                    }
+                    zring[warp + 1][j % ZRS] = zbot;
+                    mring[warp + 1][j % ZRS] = mbot;
                 }
+                if (((j + 1) % CHS) == 0 || j == ncols - 1)
+                    if (lane == 31) st_release_cta(&prog[warp + 1], (int)(j + 1));
+            } else if (to_global) {
+                if (lane == 31) {
+                    grow_out[j] = zbot;
+                    gmrow_out[j] = mbot;
+                }
+                if (((j + 1) & (args.chg - 1)) == 0 || j == ncols - 1)
+                    if (lane == 31) st_release_gpu(args.gprog + b, gbase_out + j + 1);
+            }
+        };
+        auto load_col = [&](int64_t j, R (&vb)[D]) {
+            const int slot = (int)(j & (RING_COLS - 1));
+#pragma unroll
+            for (int k = 0; k < D; ++k) vb[k] = ring.v[slot * D + k];
+        };
+
+        Z zbot = INF;
+        R mbot = R(0);
+        // Generic step (pipeline fill / drain): lanes outside [0, ncols) idle.
+        auto generic = [&](int64_t st) {
+            preamble(st);
+            Z zup = __shfl_up_sync(FULL, zbot, 1);
+            R mup = __shfl_up_sync(FULL, mbot, 1);
+            const int64_t j = st - lane;
+            Z zpn = zup;
+            if (st < ncols) top_input(st, zup, mup, zpn);
+            if (j >= 0 && j < ncols) {
+                R vb[D];
+                load_col(j, vb);
+                const int slot = (int)(j & (RING_COLS - 1));
+                zbot = L.step(vb, ring.t[slot], ring.del[slot], zup, mup, j == 0, args.nu, args.p,
+                              mbot, zpn);
                 if (owner && j == ncols - 1) args.out[0] = L.z_at(own_q);
             }
+            if (st >= 31 && st - 31 < ncols) bottom_output(st, zbot, mbot);
+        };
+
+        const int64_t nsteps = ncols + 31;
+        const int64_t main_end = max((int64_t)31, ncols);  // steps [31, ncols): all lanes busy
+        int64_t st = 0;
+        for (; st < min((int64_t)31, nsteps); ++st) generic(st);
+        if (st < main_end) {
+            // Steady state, software-pipelined: the distances of column j+1
+            // are computed while the z recurrence of column j runs.
+            R mn[K];
+            {
+                R vb[D];
+                load_col(st - lane, vb);
+                L.dists(vb, args.p, mn);
+            }
+            for (; st < main_end; ++st) {
+                preamble(st);
+                Z zup = __shfl_up_sync(FULL, zbot, 1);
+                R mup = __shfl_up_sync(FULL, mbot, 1);
+                Z zpn = zup;
+                top_input(st, zup, mup, zpn);
+                const int64_t j = st - lane;
+                const int slot = (int)(j & (RING_COLS - 1));
+                zbot = L.chain(mn, ring.t[slot], ring.del[slot], zup, mup, j == 0, args.nu, mbot,
+                               zpn);
+                if (owner && j == ncols - 1) args.out[0] = L.z_at(own_q);
+                R vb[D];
+                load_col(j + 1, vb);
+                L.dists(vb, args.p, mn);
+                bottom_output(st, zbot, mbot);
+            }
         }
+        for (; st < nsteps; ++st) generic(st);
         cp_async_wait<0>();
         __syncwarp();
     }

@@ -149,10 +149,9 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
     a.p = pr.p;
     a.out = pr.out;
     a.gbuf = (Z*)alloc.get(sizeof(Z) * (size_t)G * (size_t)(pr.nB + 1));
-    constexpr bool shuf = LaneRows<D, K, P, E, N1, R, Z>::SHUF_M;
-    a.gmbuf = shuf ? (R*)alloc.get(sizeof(R) * (size_t)G * (size_t)(pr.nB + 1)) : nullptr;
+    a.gmbuf = (R*)alloc.get(sizeof(R) * (size_t)G * (size_t)(pr.nB + 1));
     a.gprog = (long long*)alloc.get(sizeof(long long) * (size_t)G);
-    if (!a.gbuf || !a.gprog || (shuf && !a.gmbuf)) return cudaErrorMemoryAllocation;
+    if (!a.gbuf || !a.gprog || !a.gmbuf) return cudaErrorMemoryAllocation;
     e = cudaMemsetAsync(a.gprog, 0, sizeof(long long) * (size_t)G, st);
     if (e != cudaSuccess) return e;
     void* params[] = {(void*)&a};

@@ -2,6 +2,7 @@
 //
 // Layout (device memory), the reference's PreparedSeries (core.py:177-234):
 //   V   (rows, D) row-major, row 0 of each series the zero vector   [type R]
+//                 -- +inf in the DP kernels' copy (see COL0_BY_INF)
 //   Tm  (rows)    timestamps, row 0 = 0                              [type R]
 //   Del (rows)    deletion costs, row 0 = +inf                        [type Z]
 // Series lists are packed back to back; series k occupies prepared rows
@@ -152,18 +153,29 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 // z_diag + (c(r, j) + c(r-1, j-1)) -- the same terms regrouped, 3 adds per cell
 // instead of 5, and sums of squares use FMA.
 //
-// SHUF_M: the d_prev (fp64) / c (fp32) of the lane's first row is the value
-// the lane above computed for its last row two steps earlier; it arrives by
-// shuffle (or through the warp/CTA boundary rings) instead of being
-// recomputed. Same value, same bits.
-// SPLIT_SQRT (fp64, d >= 2, degree 2): the K square roots of a step run as
+// d_prev (fp64) / c (fp32) of the lane's first row is the value the lane above
+// computed for its last row two steps earlier; it arrives by shuffle (or
+// through the warp/CTA boundary rings) instead of being recomputed. Same value,
+// same bits.
+// SPLIT_SQRT (fp64, d >= 2, degree 2): the K square roots of a column run as
 // straight-line sqrt_fast (interleavable), with one rare fix-up branch per
-// step for out-of-range arguments (twb_device.cuh).
+// column for out-of-range arguments (twb_device.cuh).
+// COL0_BY_INF (every proven-safe mode): the DP kernels' prepared virtual row 0
+// holds +inf values (prepare_kernel), so at a virtual column all three
+// candidates are already +inf and no per-cell select is needed; the caller
+// feeds zup = +inf above row 1 and zupp_next = 0 after the virtual column
+// (z(0, 0) = 0 is the diagonal of cell (1, 1)). The d / c values computed
+// against the virtual column (+inf, or NaN for infinite inputs) only ever meet
+// z_diag = z(r, 0) = +inf, whose match candidate is never selected.
+//
+// The work of one column is split in two so kernels can software-pipeline it:
+// dists() (the K local distances, independent of the wavefront) and chain()
+// (the K-row min recurrence that carries z down the lane's rows).
 template <int D, int K, int P, bool EXACT_NAN, bool NU1, typename R, typename Z>
 struct LaneRows {
     static constexpr bool F32 = sizeof(R) == 4;
-    static constexpr bool SHUF_M = D >= 2 || F32;
     static constexpr bool SPLIT_SQRT = !F32 && D >= 2 && P == 2;
+    static constexpr bool COL0_BY_INF = !EXACT_NAN;
     R a[K][D];
     R ta[K];
     Z da[K];
@@ -171,11 +183,9 @@ struct LaneRows {
     R mr[K];  // fp64: d(r, j-1); fp32: c(r, j-1)
     R gr[K];  // fp64: t_a(r) - t_b(j-1) (signed, |.| at use)
     Z zupp;   // z(r0-1, j-1)
-    R mupp;   // d(r0-1, j-1) / c(r0-1, j-1) (SHUF_M)
-    R aup[D];
-    R tup;
-    R vbp[D];  // column j-1 values (top-row recompute, !SHUF_M)
-    R tbp;
+    R mupp;   // d(r0-1, j-1) / c(r0-1, j-1)
+    R tup;    // t_a(r0-1)
+    R tbp;    // t_b(j-1)
 
     // Rows [r0, r0+K) of the prepared series at `base`; rows > n are zero
     // (computed, never read back).
@@ -192,13 +202,7 @@ struct LaneRows {
             da[q] = ok ? A.del[g] : Z(0);
         }
         const int64_t ru = r0 - 1;
-        const bool oku = ru <= n;
-        const int64_t gu = base + (oku ? ru : 0);
-#pragma unroll
-        for (int k = 0; k < D; ++k) aup[k] = oku ? A.v[gu * D + k] : R(0);
-        tup = oku ? A.t[gu] : R(0);
-#pragma unroll
-        for (int k = 0; k < D; ++k) vbp[k] = R(0);
+        tup = ru <= n ? A.t[base + ru] : R(0);
         tbp = R(0);
         zupp = zinf<Z>();
         mupp = R(0);
@@ -245,21 +249,12 @@ struct LaneRows {
         }
     }
 
-    // One column j for the K rows (interior_cost, _kernels.py:61-80, per row).
-    // zup = z(r0-1, j); mup = d(r0-1, j) / c(r0-1, j) (SHUF_M; used one step
-    // later). col0: j is a virtual column 0 (z(r, 0) = +inf, r >= 1).
+    // The K-row recurrence of column j (interior_cost, _kernels.py:61-80, per
+    // row) given mn = dists(column j). zup = z(r0-1, j); mup = d / c of row
+    // r0-1 at j (kept for the next column); col0: j is a virtual column 0.
     // Returns z(r0+K-1, j); mbot = d / c of row r0+K-1 at j.
-    //
-    // COL0_BY_INF (fp32 batch, proven-safe inputs): the prepared virtual row 0
-    // of every series holds +inf values (prepare_kernel), so at a virtual
-    // column all three candidates are already +inf and no per-cell select is
-    // needed; the caller feeds zup = +inf above row 1 and zupp_next = 0 after
-    // the virtual column (z(0, 0) = 0 is the diagonal of cell (1, 1)).
-    static constexpr bool COL0_BY_INF = F32 && sizeof(Z) == 4 && !EXACT_NAN;
-    __device__ __forceinline__ Z step(const R (&vb)[D], R tb, Z delb, Z zup, R mup, bool col0,
-                                      double nu, int p, R& mbot, Z zupp_next) {
-        R mn[K];
-        dists(vb, p, mn);
+    __device__ __forceinline__ Z chain(const R (&mn)[K], R tb, Z delb, Z zup, R mup, bool col0,
+                                       double nu, R& mbot, Z zupp_next) {
         const Z INF = zinf<Z>();
         Z zu = zup;
         Z zd = zupp;
@@ -285,12 +280,7 @@ struct LaneRows {
                 mr[q] = c;
             }
         } else {
-            // d(r0-1, j-1) and t_a(r0-1) - t_b(j-1): the values the lane above
-            // computed two steps earlier (SHUF_M) or the same operations on
-            // the same inputs (bit-identical recompute).
-            R m_up;
-            if constexpr (SHUF_M) m_up = mupp;
-            else m_up = dist<D, P, R>(aup, vbp, p);
+            R m_up = mupp;
             R g_up = tup - tbp;
 #pragma unroll
             for (int q = 0; q < K; ++q) {
@@ -303,7 +293,7 @@ struct LaneRows {
                 const Z del_b = zl[q] + delb;
                 const Z del_a = zu + da[q];
                 Z z = cell_min<EXACT_NAN>(del_a, del_b, match);
-                z = col0 ? INF : z;
+                if constexpr (!COL0_BY_INF) z = col0 ? INF : z;
                 zd = zl[q];
                 zl[q] = z;
                 zu = z;
@@ -315,13 +305,16 @@ struct LaneRows {
         }
         zupp = zupp_next;
         mupp = mup;
-        if constexpr (!SHUF_M) {
-#pragma unroll
-            for (int k = 0; k < D; ++k) vbp[k] = vb[k];
-        }
         tbp = tb;
         mbot = mr[K - 1];
         return zu;
+    }
+
+    __device__ __forceinline__ Z step(const R (&vb)[D], R tb, Z delb, Z zup, R mup, bool col0,
+                                      double nu, int p, R& mbot, Z zupp_next) {
+        R mn[K];
+        dists(vb, p, mn);
+        return chain(mn, tb, delb, zup, mup, col0, nu, mbot, zupp_next);
     }
 
     // z of row slot q (runtime index) without local-memory indexing.
