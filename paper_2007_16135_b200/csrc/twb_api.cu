@@ -268,7 +268,7 @@ int twed_pair_dev(const T* dA, int64_t nA, const T* dTA, const T* dB, int64_t nB
     // order-free (not in the NaN-exact mode).
     int ra = 0, rb = 1;
     int64_t na = nA, nb = nB;
-    if (!v.E && nB > nA) {
+    if (!v.E && nB > nA && !getenv("TWB_NO_SWAP")) {  // env: tuning experiments
         ra = 1;
         rb = 0;
         std::swap(na, nb);

@@ -487,31 +487,53 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         const int64_t main_end = max((int64_t)31, ncols);  // steps [31, ncols): all lanes busy
         int64_t st = 0;
         for (; st < min((int64_t)31, nsteps); ++st) generic(st);
-        if (st < main_end) {
-            // Steady state, software-pipelined: the distances of column j+1
-            // are computed while the z recurrence of column j runs.
-            R mn[K];
+        if (!EXACT_NAN && st < main_end) {
+            // Steady state, software-pipelined: chain2 of column j and the
+            // distances + prep of column j+1 form one basic block.
+            Z pre[K];
+            R tbj;
             {
+                const int64_t j = st - lane;
                 R vb[D];
-                load_col(st - lane, vb);
-                L.dists(vb, args.p, mn);
+                load_col(j, vb);
+                const int slot = (int)(j & (RING_COLS - 1));
+                R mn[K];
+                L.dists_safe(vb, args.p, mn);
+                tbj = ring.t[slot];
+                L.prep(mn, tbj, ring.del[slot], L.zupp, L.mupp, L.tbp, args.nu, pre);
             }
-            for (; st < main_end; ++st) {
+            Z zpn = INF;
+            R mup = R(0);
+            // one steady-state step; with_next = false on the last one leaves
+            // the state at column j for the generic drain steps.
+            auto main_step = [&](bool with_next) {
                 preamble(st);
                 Z zup = __shfl_up_sync(FULL, zbot, 1);
-                R mup = __shfl_up_sync(FULL, mbot, 1);
-                Z zpn = zup;
+                mup = __shfl_up_sync(FULL, mbot, 1);
+                zpn = zup;
                 top_input(st, zup, mup, zpn);
                 const int64_t j = st - lane;
-                const int slot = (int)(j & (RING_COLS - 1));
-                zbot = L.chain(mn, ring.t[slot], ring.del[slot], zup, mup, j == 0, args.nu, mbot,
-                               zpn);
+                zbot = L.chain2(pre, zup);
+                mbot = L.mr[K - 1];
                 if (owner && j == ncols - 1) args.out[0] = L.z_at(own_q);
-                R vb[D];
-                load_col(j + 1, vb);
-                L.dists(vb, args.p, mn);
+                if (with_next) {  // column j+1
+                    R vb[D];
+                    load_col(j + 1, vb);
+                    const int slot = (int)((j + 1) & (RING_COLS - 1));
+                    R mn[K];
+                    L.dists_safe(vb, args.p, mn);
+                    const R tbn = ring.t[slot];
+                    L.prep(mn, tbn, ring.del[slot], zpn, mup, tbj, args.nu, pre);
+                    tbj = tbn;
+                }
                 bottom_output(st, zbot, mbot);
-            }
+            };
+            for (; st < main_end - 1; ++st) main_step(true);
+            main_step(false);
+            ++st;
+            L.zupp = zpn;  // z(r0-1, j), d(r0-1, j), t_b(j) of the last column
+            L.mupp = mup;
+            L.tbp = tbj;
         }
         for (; st < nsteps; ++st) generic(st);
         cp_async_wait<0>();

@@ -310,6 +310,79 @@ struct LaneRows {
         return zu;
     }
 
+    // ---- split form of the proven-safe recurrence (software pipelining) ----
+    // In safe mode min is order-free, so cell (r, j) = min(del_a, pre) with
+    // pre = min(match, del_b) computable before z(r-1, j) is known:
+    //   prep(j) needs column j's distances and the column j-1 state
+    //   (z, d, t-gap of rows r0-1 .. r0+K-1), chain2(j) needs pre and z(r0-1, j).
+    // The kernels run chain2(j) and dists(j+1) + prep(j+1) in the same basic
+    // block so the K-row recurrence overlaps the next column's arithmetic.
+
+    // Straight-line distances (fp64 safe mode: sqrt_safe, no branch).
+    __device__ __forceinline__ void dists_safe(const R (&vb)[D], int p, R (&mn)[K]) const {
+        if constexpr (SPLIT_SQRT) {
+#pragma unroll
+            for (int q = 0; q < K; ++q) mn[q] = sqrt_safe(sumsq<D>(a[q], vb));
+        } else {
+            dists(vb, p, mn);
+        }
+    }
+
+    // pre[q] = min(match(r, j), del_b(r, j)) for the K rows; z of column j-1
+    // in zl, zd0 = z(r0-1, j-1), m0 = d / c(r0-1, j-1), tbprev = t_b(j-1).
+    // Updates mr / gr to column j.
+    __device__ __forceinline__ void prep(const R (&mn)[K], R tb, Z delb, Z zd0, R m0, R tbprev,
+                                         double nu, Z (&pre)[K]) {
+        if constexpr (F32) {
+            const float nuf = (float)nu;
+#pragma unroll
+            for (int q = K - 1; q >= 0; --q) {
+                const float g = ta[q] - tb;
+                const float c = NU1 ? mn[q] + fabsf(g) : __fmaf_rn(nuf, fabsf(g), mn[q]);
+                const float c_up = q > 0 ? mr[q - 1] : m0;
+                const Z zd = q > 0 ? zl[q - 1] : zd0;
+                const float w = c + c_up;
+                Z match;
+                if constexpr (sizeof(Z) == 4) match = zd + w;
+                else match = zd + (double)w;
+                const Z del_b = zl[q] + delb;
+                pre[q] = sizeof(Z) == 4 ? (Z)fminf((float)match, (float)del_b)
+                                        : (match < del_b ? match : del_b);
+                mr[q] = c;
+            }
+        } else {
+#pragma unroll
+            for (int q = K - 1; q >= 0; --q) {
+                const R g = ta[q] - tb;
+                const R g_up = q > 0 ? gr[q - 1] : tup - tbprev;
+                const R m_up = q > 0 ? mr[q - 1] : m0;
+                const Z zd = q > 0 ? zl[q - 1] : zd0;
+                const double gs = __dadd_rn(fabs(g), fabs(g_up));
+                const double tt = NU1 ? gs : __dmul_rn(nu, gs);
+                const Z match = __dadd_rn(__dadd_rn(__dadd_rn(zd, mn[q]), m_up), tt);
+                const Z del_b = zl[q] + delb;
+                pre[q] = match < del_b ? match : del_b;
+                mr[q] = mn[q];
+                gr[q] = g;
+            }
+        }
+    }
+
+    // The K-row recurrence z(r, j) = min(z(r-1, j) + del_a(r), pre[r]).
+    __device__ __forceinline__ Z chain2(const Z (&pre)[K], Z zup) {
+        Z zu = zup;
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+            const Z del_a = zu + da[q];
+            Z z;
+            if constexpr (sizeof(Z) == 4) z = fminf(pre[q], del_a);
+            else z = pre[q] < del_a ? pre[q] : del_a;
+            zl[q] = z;
+            zu = z;
+        }
+        return zu;
+    }
+
     __device__ __forceinline__ Z step(const R (&vb)[D], R tb, Z delb, Z zup, R mup, bool col0,
                                       double nu, int p, R& mbot, Z zupp_next) {
         R mn[K];

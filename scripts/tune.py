@@ -40,6 +40,24 @@ if kind == "pair":
         k = min(ks)
         print(f"pair n={n} d={d} {dt} ws={ws}: {k:.3f} ms  {n*n/k/1e6:.1f} GCUPS  "
               f"result={out.item()!r}", flush=True)
+elif kind == "pair2":  # pair2 nA nB d dtype [reps]: rows nA (TWB_NO_SWAP set)
+    os.environ["TWB_NO_SWAP"] = "1"
+    na, nb, d, dt = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), sys.argv[5]
+    npdt = np.float32 if dt == "f32" else np.float64
+    rng = np.random.default_rng(3)
+    a = torch.from_numpy(np.cumsum(rng.standard_normal((na, d)), 0).astype(npdt)).to(dev)
+    b = torch.from_numpy(np.cumsum(rng.standard_normal((nb, d)), 0).astype(npdt)).to(dev)
+    ta = torch.arange(na, dtype=a.dtype, device=dev)
+    tb = torch.arange(nb, dtype=a.dtype, device=dev)
+    out = twb.twed_dev(a, ta, b, tb, nu=1.0, lamb=1.0, degree=2)
+    lib.twb_last_kernel_ms()
+    ks = []
+    for _ in range(2):
+        twb.twed_dev(a, ta, b, tb, nu=1.0, lamb=1.0, degree=2, out=out)
+        ks.append(lib.twb_last_kernel_ms())
+    k = min(ks)
+    print(f"pair2 nA={na} nB={nb} d={d} {dt} cfg={os.environ.get('TWB_WAVE_CFG')}: {k:.3f} ms "
+          f"{na*nb/k/1e6:.2f} GCUPS  {k*1e-3*1.965e9/nb:.0f} cycles/column", flush=True)
 else:
     N, n, d, dt, tri = int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4]), sys.argv[5], \
         sys.argv[6] == "1"
