@@ -90,10 +90,12 @@ void init_pool(int dev) {
 // negative-signed, the DP min is order-free and exact symmetry allows
 // swapping the pair. Otherwise the NaN-exact compare chain is used.
 // ---------------------------------------------------------------------------
-// tiny > 0 (fp32 values): nonzero |x| < tiny also counts as unsafe, because
-// the fp32 kernels take the square root with flush-to-zero (sqrt.approx.ftz)
-// on the safe path; with every nonzero |x| >= 2^-30 a nonzero sum of squared
-// differences is >= 2^-106, far above the fp32 denormal range.
+// tiny > 0 (values): nonzero |x| < tiny also counts as unsafe. fp32: the
+// kernels take the square root with flush-to-zero (sqrt.approx.ftz) on the
+// safe path; with every nonzero |x| >= 2^-30 a nonzero sum of squared
+// differences is >= 2^-106, far above the fp32 denormal range. fp64 (tiny =
+// 2^-400): a nonzero sum is >= 2^-904, inside the branch-free sqrt's range
+// (twb_device.cuh sqrt_fast0).
 template <typename T>
 __global__ void unsafe_kernel(const T* __restrict__ x, int64_t n, double limit, double tiny,
                               int* flag) {
@@ -227,7 +229,7 @@ constexpr double safe_limit() {
 }
 template <typename R>
 constexpr double safe_tiny() {
-    return sizeof(R) == 8 ? 0.0 : 0x1p-30;
+    return sizeof(R) == 8 ? 0x1p-400 : 0x1p-30;
 }
 
 // ---------------------------------------------------------------------------
@@ -835,7 +837,9 @@ int twb_band_solve_f64(const double* va, const double* ta, const double* dela, i
     const double lim = safe_limit<double>();
     for (int k = 0; k < 6; ++k) {
         const bool is_del = k == 2 || k == 5;  // del[0] = +inf by construction
-        check_unsafe(d[k] + (is_del ? 1 : 0), n[k] - (is_del ? 1 : 0), lim, dflag, st);
+        const bool is_val = k == 0 || k == 3;
+        check_unsafe(d[k] + (is_del ? 1 : 0), n[k] - (is_del ? 1 : 0), lim, dflag, st,
+                     is_val ? safe_tiny<double>() : 0.0);
     }
     // the DP kernels' copy marks the virtual row 0 with +inf (COL0_BY_INF)
     static const double infs[4] = {HUGE_VAL, HUGE_VAL, HUGE_VAL, HUGE_VAL};

@@ -178,6 +178,8 @@ cudaError_t run_wave(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream
             if (c == "k4w16") return run_wave_cfg<D, 4, P, E, N1, 16, 1, R, Z>(pr, alloc, st, ctx);
             if (c == "k2w8") return run_wave_cfg<D, 2, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
             if (c == "k8w4x2") return run_wave_cfg<D, 8, P, E, N1, 4, 2, R, Z>(pr, alloc, st, ctx);
+            if (c == "k6w12") return run_wave_cfg<D, 6, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k6w6x2") return run_wave_cfg<D, 6, P, E, N1, 6, 2, R, Z>(pr, alloc, st, ctx);
         }
     }
     // Long row side: 8 rows per lane (2048-row stripes). Otherwise 2 rows per

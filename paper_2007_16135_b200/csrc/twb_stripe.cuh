@@ -318,11 +318,13 @@ struct LaneRows {
     // The kernels run chain2(j) and dists(j+1) + prep(j+1) in the same basic
     // block so the K-row recurrence overlaps the next column's arithmetic.
 
-    // Straight-line distances (fp64 safe mode: sqrt_safe, no branch).
+    // Straight-line distances (fp64 safe mode: sqrt_fast0, no branch; the
+    // +inf virtual column gives NaN distances there, which only ever meet
+    // z_diag = +inf and lose every min: pre = del_b, as with +inf).
     __device__ __forceinline__ void dists_safe(const R (&vb)[D], int p, R (&mn)[K]) const {
         if constexpr (SPLIT_SQRT) {
 #pragma unroll
-            for (int q = 0; q < K; ++q) mn[q] = sqrt_safe(sumsq<D>(a[q], vb));
+            for (int q = 0; q < K; ++q) mn[q] = sqrt_fast0(sumsq<D>(a[q], vb));
         } else {
             dists(vb, p, mn);
         }
