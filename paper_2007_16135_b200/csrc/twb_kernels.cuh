@@ -274,11 +274,11 @@ template <int D, typename R, typename Z>
 __host__ __device__ constexpr size_t wave_smem_rings(int warps) {
     return (sizeof(ColRing<D, R, Z>) * warps + 15) / 16 * 16;
 }
-// rings | zring[W][ZRS] | mring[W][ZRS] | gstage z[64] | gstage m[64] | prog[W] | cons[W]
+// rings | zring[W][ZRS] | mring[W][ZRS] | gstage z[ZRS] | gstage m[ZRS] | prog[W] | cons[W]
 template <int D, typename R, typename Z>
 __host__ __device__ constexpr size_t wave_smem(int warps) {
-    return wave_smem_rings<D, R, Z>(warps) + sizeof(Z) * (ZRS * warps + 64) +
-           sizeof(R) * (ZRS * warps + 64) + sizeof(int) * 2 * warps;
+    return wave_smem_rings<D, R, Z>(warps) + sizeof(Z) * (ZRS * warps + ZRS) +
+           sizeof(R) * (ZRS * warps + ZRS) + sizeof(int) * 2 * warps;
 }
 
 template <typename R, typename Z>
@@ -306,10 +306,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
     p0 += sizeof(Z) * ZRS * WARPS;
     auto* mring = reinterpret_cast<R(*)[ZRS]>(p0);
     p0 += sizeof(R) * ZRS * WARPS;
-    Z* gstage = reinterpret_cast<Z*>(p0);
-    p0 += sizeof(Z) * 64;
+    Z* gstage = reinterpret_cast<Z*>(p0);  // warp 0's row-above ring (global input / row 0)
+    p0 += sizeof(Z) * ZRS;
     R* gmstage = reinterpret_cast<R*>(p0);
-    p0 += sizeof(R) * 64;
+    p0 += sizeof(R) * ZRS;
     int* prog = reinterpret_cast<int*>(p0);
     int* cons = prog + WARPS;
     const int warp = threadIdx.x >> 5;
@@ -386,8 +386,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                 if (from_global && st < ncols) {
                     const int64_t c = st + lane;
                     if (c < ncols) {
-                        gstage[c & 63] = pz;
-                        gmstage[c & 63] = pm;
+                        gstage[c % ZRS] = pz;
+                        gmstage[c % ZRS] = pm;
                     }
                     if (st + 32 < ncols) fetch(st + 32);
                     __syncwarp();
@@ -427,8 +427,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                 }
                 mt = R(0);
             } else {
-                zt = gstage[st & 63];
-                mt = gmstage[st & 63];
+                zt = gstage[st % ZRS];
+                mt = gmstage[st % ZRS];
                 pn = zt;
             }
             if (lane == 0) {
@@ -484,56 +484,101 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         };
 
         const int64_t nsteps = ncols + 31;
-        const int64_t main_end = max((int64_t)31, ncols);  // steps [31, ncols): all lanes busy
         int64_t st = 0;
         for (; st < min((int64_t)31, nsteps); ++st) generic(st);
-        if (!EXACT_NAN && st < main_end) {
-            // Steady state, software-pipelined: chain2 of column j and the
-            // distances + prep of column j+1 form one basic block.
+        // Steady state (safe modes), software-pipelined: chain2 of column j and
+        // the distances + prep of column j+1 form one basic block. Groups of
+        // CHS steps in which every lane is busy run a branch-free body with flow
+        // control once per group; the drain runs the same step lane-predicated.
+        for (; st < min((int64_t)32, nsteps); ++st) generic(st);
+        if (!EXACT_NAN && st < nsteps) {
+            if (warp == 0 && top_boundary) {  // row 0 for st >= 32: z = +inf, d = 0
+                for (int c = lane; c < ZRS; c += 32) {
+                    gstage[c] = INF;
+                    gmstage[c] = R(0);
+                }
+                __syncwarp();
+            }
+            const Z* tz = warp > 0 ? zring[warp] : gstage;
+            const R* tm = warp > 0 ? mring[warp] : gmstage;
+            // lane 31's output: next warp's ring, the global boundary row, or
+            // a dummy slot (last stripe's last warp); generic pointers
+            Z* oz = to_ring ? zring[warp + 1] : (to_global ? grow_out : gstage);
+            R* om = to_ring ? mring[warp + 1] : (to_global ? gmrow_out : gmstage);
+            const int omask = to_ring ? ZRS - 1 : (to_global ? 0x7fffffff : 0);
+            const bool ow = lane == 31 && (to_ring || to_global);
             Z pre[K];
             R tbj;
             {
-                const int64_t j = st - lane;
+                const int j = (int)st - lane;
                 R vb[D];
                 load_col(j, vb);
-                const int slot = (int)(j & (RING_COLS - 1));
+                const int slot = j & (RING_COLS - 1);
                 R mn[K];
                 L.dists_safe(vb, args.p, mn);
                 tbj = ring.t[slot];
                 L.prep(mn, tbj, ring.del[slot], L.zupp, L.mupp, L.tbp, args.nu, pre);
             }
-            Z zpn = INF;
-            R mup = R(0);
-            // one steady-state step; with_next = false on the last one leaves
-            // the state at column j for the generic drain steps.
-            auto main_step = [&](bool with_next) {
-                preamble(st);
+            auto body = [&](int t, bool check) {  // check = false: all lanes busy
                 Z zup = __shfl_up_sync(FULL, zbot, 1);
-                mup = __shfl_up_sync(FULL, mbot, 1);
-                zpn = zup;
-                top_input(st, zup, mup, zpn);
-                const int64_t j = st - lane;
-                zbot = L.chain2(pre, zup);
-                mbot = L.mr[K - 1];
-                if (owner && j == ncols - 1) args.out[0] = L.z_at(own_q);
-                if (with_next) {  // column j+1
+                R mup = __shfl_up_sync(FULL, mbot, 1);
+                const Z zt = tz[t % ZRS];
+                const R mt = tm[t % ZRS];
+                zup = lane == 0 ? zt : zup;
+                mup = lane == 0 ? mt : mup;
+                const int j = t - lane;
+                if (!check || j < ncols) {
+                    zbot = L.chain2(pre, zup);
+                    mbot = L.mr[K - 1];
+                    if (check && owner && j == ncols - 1) args.out[0] = L.z_at(own_q);
                     R vb[D];
                     load_col(j + 1, vb);
-                    const int slot = (int)((j + 1) & (RING_COLS - 1));
+                    const int slot = (j + 1) & (RING_COLS - 1);
                     R mn[K];
                     L.dists_safe(vb, args.p, mn);
                     const R tbn = ring.t[slot];
-                    L.prep(mn, tbn, ring.del[slot], zpn, mup, tbj, args.nu, pre);
+                    L.prep(mn, tbn, ring.del[slot], zup, mup, tbj, args.nu, pre);
                     tbj = tbn;
                 }
-                bottom_output(st, zbot, mbot);
+                if (ow && (!check || t - 31 < ncols)) {
+                    oz[(t - 31) & omask] = zbot;
+                    om[(t - 31) & omask] = mbot;
+                }
             };
-            for (; st < main_end - 1; ++st) main_step(true);
-            main_step(false);
-            ++st;
-            L.zupp = zpn;  // z(r0-1, j), d(r0-1, j), t_b(j) of the last column
-            L.mupp = mup;
-            L.tbp = tbj;
+            // full groups: every step t of the group has all lanes in [0, ncols - 1)
+            while (st + CHS < ncols) {
+                const int st0 = (int)st;
+                preamble(st);
+                if (to_ring) {  // lane 31 writes columns <= st0 - 16 this group
+                    const int need = st0 - 16 - ZRS + 1;
+                    while (ld_acquire_cta(&cons[warp + 1]) < need) {
+                    }
+                }
+#pragma unroll 1
+                for (int i = 0; i < CHS; ++i) body(st0 + i, false);
+                st += CHS;
+                const int done = (int)st - 31;  // lane 31 finished columns [0, done)
+                if (to_ring) {
+                    if (lane == 31) st_release_cta(&prog[warp + 1], done);
+                } else if (to_global && ((done & (args.chg - 1)) < CHS)) {
+                    if (lane == 31) st_release_gpu(args.gprog + b, gbase_out + done);
+                }
+            }
+            // drain: per-step flow control, lanes predicated on their column
+            for (; st < nsteps; ++st) {
+                preamble(st);
+                body((int)st, true);
+                const int64_t j31 = st - 31;
+                if (j31 >= 0 && j31 < ncols) {
+                    if (to_ring) {
+                        if (((j31 + 1) % CHS) == 0 || j31 == ncols - 1)
+                            if (lane == 31) st_release_cta(&prog[warp + 1], (int)(j31 + 1));
+                    } else if (to_global) {
+                        if (((j31 + 1) & (args.chg - 1)) == 0 || j31 == ncols - 1)
+                            if (lane == 31) st_release_gpu(args.gprog + b, gbase_out + j31 + 1);
+                    }
+                }
+            }
         }
         for (; st < nsteps; ++st) generic(st);
         cp_async_wait<0>();
