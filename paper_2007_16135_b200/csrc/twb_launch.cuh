@@ -168,18 +168,18 @@ cudaError_t run_wave(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream
     int sms = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // TWB_WAVE_CFG pins a variant (tuning experiments, fp64 d = 3 only):
-    // k8w8 | k4w8x2 (two CTAs per SM) | k4w16 | k2w8 | k8w4x2
-    if constexpr (D == 3 && sizeof(R) == 8 && !E) {
+    // TWB_WAVE_CFG pins a variant (tuning experiments; proven-safe modes):
+    // k<rows per lane>w<warps per CTA>[x<CTAs per SM>]
+    if constexpr (!E) {
         if (const char* env = getenv("TWB_WAVE_CFG")) {
             const std::string c(env);
             if (c == "k8w8") return run_wave_cfg<D, 8, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k4w8x2") return run_wave_cfg<D, 4, P, E, N1, 8, 2, R, Z>(pr, alloc, st, ctx);
-            if (c == "k4w16") return run_wave_cfg<D, 4, P, E, N1, 16, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k2w8") return run_wave_cfg<D, 2, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k8w4x2") return run_wave_cfg<D, 8, P, E, N1, 4, 2, R, Z>(pr, alloc, st, ctx);
             if (c == "k6w12") return run_wave_cfg<D, 6, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k6w6x2") return run_wave_cfg<D, 6, P, E, N1, 6, 2, R, Z>(pr, alloc, st, ctx);
+            if (c == "k8w12") return run_wave_cfg<D, 8, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k4w16") return run_wave_cfg<D, 4, P, E, N1, 16, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k4w12") return run_wave_cfg<D, 4, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k2w8") return run_wave_cfg<D, 2, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k2w16") return run_wave_cfg<D, 2, P, E, N1, 16, 1, R, Z>(pr, alloc, st, ctx);
         }
     }
     // Long row side: 8 rows per lane (2048-row stripes). Otherwise 2 rows per
