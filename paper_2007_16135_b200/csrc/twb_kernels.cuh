@@ -216,12 +216,26 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
         Z zbot = INF;
         R mbot = R(0);
         const int nsteps = ncols + LW - 1;
-        for (int s = 0; s < nsteps; ++s) {
-            if ((s & 31) == 0) {
-                cp_async_wait<1>();
-                __syncwarp();
-                stage_block<D>(ring, args.B, c0, ncols, (s >> 5) + 2, lane);
+        auto stage = [&](int s) {  // s % 32 == 0
+            cp_async_wait<0>();  // the pipelined body reads one column ahead
+            __syncwarp();
+            stage_block<D>(ring, args.B, c0, ncols, (s >> 5) + 2, lane);
+        };
+        // end of a B series at this lane's column j: write the result, advance
+        auto series_end = [&](int j) {
+            const int64_t jj = j0 + sidx;
+            if (writer && (!args.tri || jj >= i)) {
+                const Z v = L.z_at(own_q);
+                orow[jj] = v;
+                if (args.mirror && jj != i) args.out[(jj - args.row_begin) * args.ld + i] = v;
             }
+            ++sidx;
+            pos = 0;
+            curlen = sidx < nser ? slen[warp][sidx] : 0;
+        };
+        // Generic step (fill / drain, NaN-exact mode): lanes outside [0, ncols) idle.
+        auto generic = [&](int s) {
+            if ((s & 31) == 0) stage(s);
             Z zup = __shfl_up_sync(FULL, zbot, 1, LW);
             R mup = __shfl_up_sync(FULL, mbot, 1, LW);
             const int j = s - hl;
@@ -245,16 +259,68 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
                     mup = R(0);
                 }
                 zbot = L.step(vb, tb, delb, zup, mup, col0, args.nu, args.p, mbot, zpn);
-                if (++pos == curlen) {
-                    const int64_t jj = j0 + sidx;
-                    if (writer && (!args.tri || jj >= i)) {
-                        const Z v = L.z_at(own_q);
-                        orow[jj] = v;
-                        if (args.mirror && jj != i) args.out[(jj - args.row_begin) * args.ld + i] = v;
+                if (++pos == curlen) series_end(j);
+            }
+        };
+        int s = 0;
+        if constexpr (EXACT_NAN) {
+            for (; s < nsteps; ++s) generic(s);
+        } else {
+            // Safe modes: after the LW-step fill, groups of 16 steps in which
+            // every lane is busy run a software-pipelined body (chain2 of
+            // column j with the distances + prep of column j+1, as in
+            // wave_kernel) with predicated series bookkeeping; the drain runs
+            // the same body lane-predicated.
+            for (; s < min(LW, nsteps); ++s) generic(s);
+            if (s < nsteps) {
+                Z pre[K];
+                R tbj;
+                {
+                    const int j = s - hl;
+                    const int slot = j & (RING_COLS - 1);
+                    R vb[D];
+#pragma unroll
+                    for (int k = 0; k < D; ++k) vb[k] = ring.v[slot * D + k];
+                    R mn[K];
+                    L.dists_safe(vb, args.p, mn);
+                    tbj = ring.t[slot];
+                    L.prep(mn, tbj, ring.del[slot], L.zupp, L.mupp, L.tbp, args.nu, pre);
+                }
+                auto body = [&](int t, bool check) {
+                    Z zup = __shfl_up_sync(FULL, zbot, 1, LW);
+                    R mup = __shfl_up_sync(FULL, mbot, 1, LW);
+                    const int j = t - hl;
+                    if (!check || j < ncols) {
+                        const bool col0 = pos == 0;
+                        // row 0 above the lane group: z(0, j) = +inf; z(0, 0) = 0
+                        // enters as the diagonal of the next column
+                        Z zpn = zup;
+                        zup = hl == 0 ? INF : zup;
+                        zpn = hl == 0 ? (col0 ? Z(0) : INF) : zpn;
+                        mup = hl == 0 ? R(0) : mup;
+                        zbot = L.chain2(pre, zup);
+                        mbot = L.mr[K - 1];
+                        const int slot = (j + 1) & (RING_COLS - 1);
+                        R vb[D];
+#pragma unroll
+                        for (int k = 0; k < D; ++k) vb[k] = ring.v[slot * D + k];
+                        R mn[K];
+                        L.dists_safe(vb, args.p, mn);
+                        const R tbn = ring.t[slot];
+                        L.prep(mn, tbn, ring.del[slot], zpn, mup, tbj, args.nu, pre);
+                        tbj = tbn;
+                        if (++pos == curlen) series_end(j);
                     }
-                    ++sidx;
-                    pos = 0;
-                    curlen = sidx < nser ? slen[warp][sidx] : 0;
+                };
+                while (s + 16 <= ncols) {  // lanes' columns s - hl .. s + 15 - hl all valid
+                    if ((s & 31) == 0) stage(s);
+#pragma unroll 1
+                    for (int u = 0; u < 16; ++u) body(s + u, false);
+                    s += 16;
+                }
+                for (; s < nsteps; ++s) {
+                    if ((s & 31) == 0) stage(s);
+                    body(s, true);
                 }
             }
         }

@@ -84,9 +84,8 @@ cudaError_t run_batch(BatchArgs<R, Z> a, int64_t max_rows, cudaStream_t st, Laun
     return cudaErrorInvalidValue;
 }
 
-// Wavefront variants: (warps, k) in {(8, 2), (8, 8)} -- picked so that the
-// row stripes cover every SM (short pairs) or amortise the per-row top-row
-// recompute (long pairs).
+// Wavefront variants (rows per lane K, warps per CTA W, CTAs per SM MINB);
+// run_wave picks one by the row-side length.
 template <int D, int K, int P, bool E, bool N1, int W, int MINB, typename R, typename Z>
 cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream_t st,
                          LaunchCtx* ctx) {
@@ -182,11 +181,14 @@ cudaError_t run_wave(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream
             if (c == "k2w16") return run_wave_cfg<D, 2, P, E, N1, 16, 1, R, Z>(pr, alloc, st, ctx);
         }
     }
-    // Long row side: 8 rows per lane (2048-row stripes). Otherwise 2 rows per
-    // lane so that the stripes still spread over the SMs.
-    if (pr.nA >= (int64_t)sms * 8 * 32 * 8 * 2)
-        return run_wave_cfg<D, 8, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
-    return run_wave_cfg<D, 2, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
+    // Long row side (>= 1.5 rounds of stripes): 12 warps x 6 rows per lane
+    // (12 warps/SM hide the FP64 latency; B200 sweep: n = 1M d = 3 fp64
+    // 395 GCUPS vs 376 for 8 x 8, d = 1 920 vs 775, fp32 mode 874 vs 507).
+    // Shorter: 8 warps x 8 rows (fewer, longer stripes: less pipeline fill;
+    // n = 300k d = 3 298 GCUPS vs 245).
+    if (pr.nA >= (int64_t)sms * 12 * 32 * 6 * 3 / 2)
+        return run_wave_cfg<D, 6, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
+    return run_wave_cfg<D, 8, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
 }
 
 }  // namespace twb
