@@ -324,7 +324,7 @@ def run_ours(args, world, rank, local):
         ev1.record(stream)
         torch.cuda.synchronize()
     barrier(world)
-    launches = _lib.take_launch_count() + args.steps  # + our L2-flush writes are torch's
+    launches = _lib.take_launch_count()  # libtwb200 kernels only (the L2 flush is torch's)
     elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1), world)
     value = world * args.steps * cells / (elapsed_ms * 1e-3) / 1e9
     ms_per_step = elapsed_ms / args.steps
@@ -428,14 +428,27 @@ def run_batch_cfg5(args, world, rank, local):
     dS = torch.from_numpy(S).to(dev)
     dT = torch.from_numpy(TS).to(dev)
     off = np.arange(N + 1, dtype=np.int64) * n
-    b0, b1 = row_bounds(N, world, True)[rank]
-    block = torch.empty((max(b1 - b0, 1), N), dtype=torch.float32, device=dev)
+    bounds = row_bounds(N, world, True)
+    b0, b1 = bounds[rank]
+    max_rows = max(e - b for b, e in bounds)
+    block = torch.zeros((max_rows, N), dtype=torch.float32, device=dev)
+    full = parts = None
+    if world > 1 and rank == 0:
+        full = torch.empty((N, N), dtype=torch.float32, device=dev)
+        parts = [torch.empty_like(block) for _ in range(world)]
     lib = _lib.load()
     lib.twb_set_kernel_timing(1)
 
     def step():
         twb.twed_batch_dev(dS, off, dT, nu=1.0, lamb=1.0, degree=2, tri=True, row_begin=b0,
-                           row_end=b1, out=block)
+                           row_end=b1, out=block[: b1 - b0])
+        if world > 1:  # the job's only collective: gather the row blocks, mirror on rank 0
+            import torch.distributed as dist
+            dist.gather(block, parts, dst=0)
+            if rank == 0:
+                for (lo, hi), part in zip(bounds, parts):
+                    full[lo:hi].copy_(part[: hi - lo])
+                twb.mirror_upper_dev(full)
 
     for _ in range(max(1, args.warmup // 2)):
         step()
@@ -458,7 +471,10 @@ def run_batch_cfg5(args, world, rank, local):
     return {"metric": "twed_batch pairs/s (tri 10k x 10k, n=128, d=2, fp32)",
             "workload": "cfg5", "pairs": pairs, "value": pairs / (ms * 1e-3), "unit": "pairs/s",
             "gcups": cells / (ms * 1e-3) / 1e9, "ms_per_step": ms, "n_gpus": world,
-            "scaling": "strong", "gather": "not timed (rows stay sharded on each GPU)",
+            "scaling": "strong",
+            "gather": ("none (one GPU: the kernel writes the mirrored matrix)" if world == 1 else
+                       "timed: NCCL gather of the row blocks to rank 0 + on-device mirror"),
+            "sharding": [list(b) for b in bounds],
             "kernel_ms": kms,
             "roofline": {"bound": "fp32", "achieved": FLOPS_PER_CELL[2] * cells / (kms * 1e-3) / 1e12,
                          "peak": peak / 1e12, "unit": "TFLOP/s",

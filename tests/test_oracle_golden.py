@@ -41,6 +41,26 @@ def test_parallel_band_matches_serial(small_golden, oracle):
         assert same_float(oracle.twed(*args, threads=4), float(case["value"])), case["name"]
 
 
+def test_tiled_schedule_matches_reference(small_golden, config_golden, oracle):
+    """orc_band_tiled (the schedule that produced the n = 1M cfg3 golden,
+    tests/golden/gen_cfg3.py) reproduces the reference's own values bit for bit."""
+    n = 0
+    for case in small_golden["pairs"]:
+        if case["degree"] > 2:
+            continue
+        args = (as_values(case["values_a"]), as_values(case["times_a"]),
+                as_values(case["values_b"]), as_values(case["times_b"]),
+                case["nu"], case["lam"], case["degree"])
+        for tile in (3, 64):
+            got = oracle.twed_tiled(*args, threads=2, tile=tile)
+            assert same_float(got, float(dec(case["value"]))), (case["name"], tile)
+        n += 1
+    assert n > 100
+    a, ta, b, tb = make_pair(3000, 3, 12)  # reference value computed by twedband itself
+    assert oracle.twed_tiled(a, ta, b, tb, 1.0, 1.0, 2, threads=4, tile=512) == \
+        config_golden["walk_3000_d3_s12"]["value"]
+
+
 def test_full_matrix_corner_matches_band(small_golden, oracle):
     for case in small_golden["pairs"][:60]:
         pa = oracle.prepare_series(as_values(case["values_a"]), as_values(case["times_a"]),
