@@ -349,7 +349,7 @@ struct LaneRows {
                 else match = zd + (double)w;
                 const Z del_b = zl[q] + delb;
                 pre[q] = sizeof(Z) == 4 ? (Z)fminf((float)match, (float)del_b)
-                                        : (match < del_b ? match : del_b);
+                                        : safe_min(match, del_b);
                 mr[q] = c;
             }
         } else {
@@ -363,7 +363,7 @@ struct LaneRows {
                 const double tt = NU1 ? gs : __dmul_rn(nu, gs);
                 const Z match = __dadd_rn(__dadd_rn(__dadd_rn(zd, mn[q]), m_up), tt);
                 const Z del_b = zl[q] + delb;
-                pre[q] = match < del_b ? match : del_b;
+                pre[q] = safe_min(match, del_b);
                 mr[q] = mn[q];
                 gr[q] = g;
             }
@@ -378,7 +378,7 @@ struct LaneRows {
             const Z del_a = zu + da[q];
             Z z;
             if constexpr (sizeof(Z) == 4) z = fminf(pre[q], del_a);
-            else z = pre[q] < del_a ? pre[q] : del_a;
+            else z = safe_min(pre[q], del_a);
             zl[q] = z;
             zu = z;
         }
