@@ -9,5 +9,5 @@ python -m pip install --no-index --no-build-isolation --no-deps --find-links /op
   --target baseline/_ref --upgrade /tmp/twb_refcopy /tmp/twb_refcopy/bindings
 rm -rf baseline/_ref_suite && mkdir -p baseline/_ref_suite
 cp -r /root/reference/pkg/tests baseline/_ref_suite/tests
-cp -r /root/reference/pkg/bindings/tests baseline/_ref_suite/bindings_tests
+mkdir -p baseline/_ref_suite/bindings && cp -r /root/reference/pkg/bindings/tests baseline/_ref_suite/bindings/tests
 echo staged
