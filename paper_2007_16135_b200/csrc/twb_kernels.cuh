@@ -332,6 +332,12 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
 // ---------------------------------------------------------------------------
 // Wavefront: one long pair.
 // ---------------------------------------------------------------------------
+// Steady-state steps per loop iteration: unrolling lets the scheduler overlap
+// one step's latency-bound z chain with the next step's distance arithmetic.
+#ifndef TWB_WAVE_UNROLL
+#define TWB_WAVE_UNROLL 2
+#endif
+constexpr int WAVE_UNROLL = TWB_WAVE_UNROLL;
 constexpr int ZRS = 256;  // shared-memory ring between consecutive warps (columns)
 constexpr int CHS = 16;   // warp-to-warp publish granularity (columns)
 constexpr int CHG = 32;   // CTA-to-CTA read granularity (columns; publish = args.chg)
@@ -620,7 +626,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                     while (ld_acquire_cta(&cons[warp + 1]) < need) {
                     }
                 }
-#pragma unroll 1
+#pragma unroll WAVE_UNROLL
                 for (int i = 0; i < CHS; ++i) body(st0 + i, false);
                 st += CHS;
                 const int done = (int)st - 31;  // lane 31 finished columns [0, done)

@@ -168,17 +168,14 @@ cudaError_t run_wave(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // TWB_WAVE_CFG pins a variant (tuning experiments; proven-safe modes):
-    // k<rows per lane>w<warps per CTA>[x<CTAs per SM>]
+    // k<rows per lane>w<warps per CTA>
     if constexpr (!E) {
         if (const char* env = getenv("TWB_WAVE_CFG")) {
             const std::string c(env);
             if (c == "k8w8") return run_wave_cfg<D, 8, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
             if (c == "k6w12") return run_wave_cfg<D, 6, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k8w12") return run_wave_cfg<D, 8, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k4w16") return run_wave_cfg<D, 4, P, E, N1, 16, 1, R, Z>(pr, alloc, st, ctx);
             if (c == "k4w12") return run_wave_cfg<D, 4, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
             if (c == "k2w8") return run_wave_cfg<D, 2, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k2w16") return run_wave_cfg<D, 2, P, E, N1, 16, 1, R, Z>(pr, alloc, st, ctx);
         }
     }
     // Long row side (>= 1.5 rounds of stripes): 12 warps x 6 rows per lane
