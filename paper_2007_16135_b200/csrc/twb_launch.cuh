@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <string>
 
@@ -113,14 +115,20 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
     // TWB_WAVE_WS=<n> pins the active warps per stripe (tuning experiments).
     int ws_pin = 0;
     if (const char* env = getenv("TWB_WAVE_WS")) ws_pin = atoi(env);
+    // Per-step time grows with the SM's load once its FP64 pipe is busy:
+    // factor max(1, ws*K*F/400)^0.75, F ~ FP64 instructions per cell (fitted
+    // to B200 sweeps, e.g. n = 100k: d = 1 best at 1024-row stripes, d = 3 at
+    // 512; n = 300k d = 3 at 1024; n = 1M at 12 x 6 rows).
+    const double F = D == 1 ? 10.0 : D == 2 ? 20.0 : D == 3 ? 24.0 : 27.0;
     for (int ws = W; ws >= 1; --ws) {
         if (ws_pin > 0 && ws != (ws_pin < W ? ws_pin : W)) continue;
         const int64_t h = (int64_t)ws * 32 * K;
         const int64_t s = (pr.nA + h - 1) / h;
         const int64_t r = (s + cap - 1) / cap;
         const int64_t g = (s + r - 1) / r;
-        const double cost = (double)r * (double)(pr.nB + 32) +
-                            (double)g * (double)(ws * (32 + CHS) + CHG) +
+        const double load = std::max(1.0, ws * K * F / 400.0);
+        const double cost = ((double)r * (double)(pr.nB + 32) +
+                             (double)g * (double)(ws * (32 + CHS) + CHG)) * pow(load, 0.75) +
                             (double)(W - ws) * 1e-6;  // ties -> more warps
         if (H == 0 || cost < best) {
             best = cost;
@@ -181,11 +189,11 @@ cudaError_t run_wave(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream
     // Long row side (>= 1.5 rounds of stripes): 12 warps x 6 rows per lane
     // (12 warps/SM hide the FP64 latency; B200 sweep: n = 1M d = 3 fp64
     // 395 GCUPS vs 376 for 8 x 8, d = 1 920 vs 775, fp32 mode 874 vs 507).
-    // Shorter: 8 warps x 8 rows (fewer, longer stripes: less pipeline fill;
-    // n = 300k d = 3 298 GCUPS vs 245).
+    // Shorter: 4 rows per lane, stripes of up to 12 warps sized by the cost
+    // model (n = 300k d = 3: 346 GCUPS; n = 100k: d = 1 331, d = 3 170).
     if (pr.nA >= (int64_t)sms * 12 * 32 * 6 * 3 / 2)
         return run_wave_cfg<D, 6, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
-    return run_wave_cfg<D, 8, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
+    return run_wave_cfg<D, 4, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
 }
 
 }  // namespace twb
