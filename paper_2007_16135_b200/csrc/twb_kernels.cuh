@@ -332,6 +332,15 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
 // ---------------------------------------------------------------------------
 // Wavefront: one long pair.
 // ---------------------------------------------------------------------------
+// A waiting warp backs off so that it does not take issue slots from the warps
+// it shares a sub-partition with (which include the one it waits for).
+#ifndef TWB_SPIN_NS
+#define TWB_SPIN_NS 0
+#endif
+__device__ __forceinline__ void spin_pause() {
+    if constexpr (TWB_SPIN_NS > 0) __nanosleep(TWB_SPIN_NS);
+}
+
 // Steady-state steps per loop iteration: unrolling lets the scheduler overlap
 // one step's latency-bound z chain with the next step's distance arithmetic.
 #ifndef TWB_WAVE_UNROLL
@@ -468,14 +477,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             if (warp > 0 && (st % CHS) == 0 && st < ncols) {
                 if (lane == 0) st_release_cta(&cons[warp], (int)st);
                 const int need = (int)min(st + CHS, ncols);
-                while (ld_acquire_cta(&prog[warp]) < need) {
-                }
+                while (ld_acquire_cta(&prog[warp]) < need) spin_pause();
             }
             const int64_t j31 = st - 31;  // lane 31's column this step
             if (to_ring && j31 >= 0 && j31 < ncols && (j31 % CHS) == 0) {
                 const int need = (int)(j31 + CHS - ZRS);
-                while (ld_acquire_cta(&cons[warp + 1]) < need) {
-                }
+                while (ld_acquire_cta(&cons[warp + 1]) < need) spin_pause();
             }
         };
         // The row above lane 0 at column st (lane 0's column), read by every
@@ -623,8 +630,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                 preamble(st);
                 if (to_ring) {  // lane 31 writes columns <= st0 - 16 this group
                     const int need = st0 - 16 - ZRS + 1;
-                    while (ld_acquire_cta(&cons[warp + 1]) < need) {
-                    }
+                    while (ld_acquire_cta(&cons[warp + 1]) < need) spin_pause();
                 }
 #pragma unroll WAVE_UNROLL
                 for (int i = 0; i < CHS; ++i) body(st0 + i, false);
