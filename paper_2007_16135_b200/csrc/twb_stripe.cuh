@@ -323,8 +323,10 @@ struct LaneRows {
     // z_diag = +inf and lose every min: pre = del_b, as with +inf).
     __device__ __forceinline__ void dists_safe(const R (&vb)[D], int p, R (&mn)[K]) const {
         if constexpr (SPLIT_SQRT) {
+            double acc[K];
 #pragma unroll
-            for (int q = 0; q < K; ++q) mn[q] = sqrt_fast0(sumsq<D>(a[q], vb));
+            for (int q = 0; q < K; ++q) acc[q] = sumsq<D>(a[q], vb);
+            sqrt_fast0_k<K>(acc, mn);
         } else {
             dists(vb, p, mn);
         }
