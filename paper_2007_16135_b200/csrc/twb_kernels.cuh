@@ -351,14 +351,17 @@ constexpr int ZRS = 256;  // shared-memory ring between consecutive warps (colum
 constexpr int CHS = 16;   // warp-to-warp publish granularity (columns)
 constexpr int CHG = 32;   // CTA-to-CTA read granularity (columns; publish = args.chg)
 
-template <int D, typename R, typename Z>
+template <int D, typename R, typename Z, int C>
+using WaveRing = ColRing<D, R, Z, RING_COLS * C>;
+
+template <int D, typename R, typename Z, int C>
 __host__ __device__ constexpr size_t wave_smem_rings(int warps) {
-    return (sizeof(ColRing<D, R, Z>) * warps + 15) / 16 * 16;
+    return (sizeof(WaveRing<D, R, Z, C>) * warps + 15) / 16 * 16;
 }
 // rings | zring[W][ZRS] | mring[W][ZRS] | gstage z[ZRS] | gstage m[ZRS] | prog[W] | cons[W]
-template <int D, typename R, typename Z>
+template <int D, typename R, typename Z, int C>
 __host__ __device__ constexpr size_t wave_smem(int warps) {
-    return wave_smem_rings<D, R, Z>(warps) + sizeof(Z) * (ZRS * warps + ZRS) +
+    return wave_smem_rings<D, R, Z, C>(warps) + sizeof(Z) * (ZRS * warps + ZRS) +
            sizeof(R) * (ZRS * warps + ZRS) + sizeof(int) * 2 * warps;
 }
 
@@ -369,7 +372,7 @@ struct WaveArgs {
     int64_t S;  // stripes
     int64_t H;  // rows per stripe
     Z* gbuf;            // gridDim.x x (nB+1): bottom row z of the CTA's current stripe
-    R* gmbuf;           // gridDim.x x (nB+1): bottom row d(r, j) (d >= 2)
+    R* gmbuf;           // gridDim.x x (nB+1): bottom row d(r, j) / c(r, j)
     long long* gprog;   // gridDim.x progress counters: stripe*(nB+1) + columns published
     int chg;            // publish granularity of the bottom row (power of 2, >= 32)
     double nu;
@@ -377,12 +380,20 @@ struct WaveArgs {
     double* out;
 };
 
-template <int D, int K, int P, bool EXACT_NAN, bool NU1, int WARPS, int MINB, typename R, typename Z>
+// Stripe sweep. C = columns per lane step: lane t at step s handles columns
+// C*(s - t) + c, c < C, so one step carries C*K cells per lane and the
+// steady-state body holds C chain2/prep pairs -- more independent work per
+// step for the same per-step latency of the warp-to-warp wavefront.
+template <int D, int K, int C, int P, bool EXACT_NAN, bool NU1, int WARPS, int MINB, typename R,
+          typename Z>
 __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R, Z> args) {
     using Lane = LaneRows<D, K, P, EXACT_NAN, NU1, R, Z>;
+    using Ring = WaveRing<D, R, Z, C>;
+    constexpr int NC = Ring::N;
+    constexpr int GCOLS = C * CHS;  // columns per group of CHS steps
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    auto* rings = reinterpret_cast<ColRing<D, R, Z>*>(smem_raw);
-    unsigned char* p0 = smem_raw + wave_smem_rings<D, R, Z>(WARPS);
+    auto* rings = reinterpret_cast<Ring*>(smem_raw);
+    unsigned char* p0 = smem_raw + wave_smem_rings<D, R, Z, C>(WARPS);
     auto* zring = reinterpret_cast<Z(*)[ZRS]>(p0);
     p0 += sizeof(Z) * ZRS * WARPS;
     auto* mring = reinterpret_cast<R(*)[ZRS]>(p0);
@@ -398,9 +409,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
     const int G = gridDim.x;
     const int b = blockIdx.x;
     const int pb = (b + G - 1) % G;
-    ColRing<D, R, Z>& ring = rings[warp];
+    Ring& ring = rings[warp];
     const Z INF = zinf<Z>();
-    const int64_t ncols = args.nB + 1;
+    const int ncols = (int)(args.nB + 1);
+    const int nsteps = (ncols + C - 1) / C + 31;
     Lane L;
 
     const int64_t s_last = (args.nA - 1) / args.H;
@@ -422,8 +434,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         if (warp >= wact) continue;
 
         L.load(args.A, 0, first_row + (int64_t)(warp * 32 + lane) * K, args.nA);
-        stage_block<D>(ring, args.B, 0, ncols, 0, lane);
-        stage_block<D>(ring, args.B, 0, ncols, 1, lane);
+        // columns [0, 64C): the first 64 steps
+#pragma unroll
+        for (int k = 0; k < 2 * C; ++k) stage_block<D>(ring, args.B, 0, ncols, k, lane);
         __syncwarp();
 
         const bool top_boundary = s == 0;                    // row 0 above warp 0
@@ -437,66 +450,70 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         R* gmrow_out = args.gmbuf + (int64_t)b * ncols;
         const R* gmrow_in = args.gmbuf + (int64_t)pb * ncols;
 
-        // Previous stripe's bottom row (warp 0 of a non-top stripe): block k =
-        // columns [32k, 32k+32) is loaded into registers one block ahead
-        // (latency hidden behind 32 steps) and parked in the 64-entry gstage
-        // ring when block k starts.
+        // Previous stripe's bottom row (warp 0 of a non-top stripe): the 32C
+        // columns of the next 32 steps are loaded into registers one block
+        // ahead (latency hidden behind 32 steps) and parked in the gstage ring.
         const bool from_global = warp == 0 && !top_boundary;
-        Z pz = Z(0);
-        R pm = R(0);
-        auto fetch = [&](int64_t c0) {  // block starting at column c0 -> registers
-            const long long need = gbase_in + min(c0 + CHG, ncols);
+        Z pz[C];
+        R pm[C];
+        auto fetch = [&](int c0) {  // columns [c0, c0 + 32C) -> registers
+            const long long need = gbase_in + min(c0 + 32 * C, ncols);
             while (ld_acquire_gpu(args.gprog + pb) < need) __nanosleep(32);
-            const int64_t c = c0 + lane;
-            if (c < ncols) {
-                pz = __ldcg(grow_in + c);
-                pm = __ldcg(gmrow_in + c);
+#pragma unroll
+            for (int k = 0; k < C; ++k) {
+                const int c = c0 + 32 * k + lane;
+                pz[k] = c < ncols ? __ldcg(grow_in + c) : Z(0);
+                pm[k] = c < ncols ? __ldcg(gmrow_in + c) : R(0);
             }
         };
         if (from_global) fetch(0);
 
         // Warp-uniform per-step bookkeeping: column staging, boundary-row
         // fetch, ring flow control with the neighbouring warps.
-        auto preamble = [&](int64_t st) {
+        auto preamble = [&](int st) {
             if ((st & 31) == 0) {
-                // wait for every staged block: the software-pipelined loop
-                // reads one column ahead, into the block staged 32 steps ago
+                // every staged block has landed; the pipelined body reads up to
+                // 2C columns past its own
                 cp_async_wait<0>();
                 __syncwarp();
-                stage_block<D>(ring, args.B, 0, ncols, (st >> 5) + 2, lane);
-                if (from_global && st < ncols) {
-                    const int64_t c = st + lane;
-                    if (c < ncols) {
-                        gstage[c % ZRS] = pz;
-                        gmstage[c % ZRS] = pm;
+#pragma unroll
+                for (int k = 0; k < C; ++k)
+                    stage_block<D>(ring, args.B, 0, ncols, (C * (st + 64)) / 32 + k, lane);
+                if (from_global && C * st < ncols) {
+#pragma unroll
+                    for (int k = 0; k < C; ++k) {
+                        const int c = C * st + 32 * k + lane;
+                        gstage[c % ZRS] = pz[k];
+                        gmstage[c % ZRS] = pm[k];
                     }
-                    if (st + 32 < ncols) fetch(st + 32);
+                    if (C * (st + 32) < ncols) fetch(C * (st + 32));
                     __syncwarp();
                 }
             }
-            if (warp > 0 && (st % CHS) == 0 && st < ncols) {
-                if (lane == 0) st_release_cta(&cons[warp], (int)st);
-                const int need = (int)min(st + CHS, ncols);
+            if (warp > 0 && (st % CHS) == 0 && C * st < ncols) {
+                if (lane == 0) st_release_cta(&cons[warp], C * st);
+                const int need = min(C * (st + CHS), ncols);
                 while (ld_acquire_cta(&prog[warp]) < need) spin_pause();
             }
-            const int64_t j31 = st - 31;  // lane 31's column this step
-            if (to_ring && j31 >= 0 && j31 < ncols && (j31 % CHS) == 0) {
-                const int need = (int)(j31 + CHS - ZRS);
+            const int j31 = C * (st - 31);  // lane 31's first column this step
+            if (to_ring && j31 >= 0 && j31 < ncols && (j31 % GCOLS) == 0) {
+                const int need = j31 + GCOLS - ZRS;
                 while (ld_acquire_cta(&cons[warp + 1]) < need) spin_pause();
             }
         };
-        // The row above lane 0 at column st (lane 0's column), read by every
-        // lane from a warp-uniform address, selected for lane 0.
-        auto top_input = [&](int64_t st, Z& zup, R& mup, Z& zpn) {
+        // The row above lane 0 at column C*st + c, read by every lane from a
+        // warp-uniform address, selected for lane 0.
+        auto top_input = [&](int st, int c, Z& zup, R& mup, Z& zpn) {
+            const int col = C * st + c;
             Z zt;
             R mt;
             Z pn;
             if (warp > 0) {
-                zt = zring[warp][st % ZRS];
-                mt = mring[warp][st % ZRS];
+                zt = zring[warp][col % ZRS];
+                mt = mring[warp][col % ZRS];
                 pn = zt;
             } else if (top_boundary) {  // row 0; d(0, j) only meets z = inf
-                const bool c0 = st == 0;
+                const bool c0 = col == 0;
                 if constexpr (Lane::COL0_BY_INF) {
                     zt = INF;
                     pn = c0 ? Z(0) : INF;
@@ -506,8 +523,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                 }
                 mt = R(0);
             } else {
-                zt = gstage[st % ZRS];
-                mt = gmstage[st % ZRS];
+                zt = gstage[col % ZRS];
+                mt = gmstage[col % ZRS];
                 pn = zt;
             }
             if (lane == 0) {
@@ -516,62 +533,87 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                 zpn = pn;
             }
         };
-        // Lane 31's bottom row at column st - 31 -> next warp / next stripe.
-        auto bottom_output = [&](int64_t st, Z zbot, R mbot) {
-            const int64_t j = st - 31;
+        // publish after lane 31 finished column j (generic / drain steps)
+        auto publish = [&](int j) {
             if (to_ring) {
-                if (lane == 31) {
-                    zring[warp + 1][j % ZRS] = zbot;
-                    mring[warp + 1][j % ZRS] = mbot;
-                }
-                if (((j + 1) % CHS) == 0 || j == ncols - 1)
-                    if (lane == 31) st_release_cta(&prog[warp + 1], (int)(j + 1));
+                if (((j + 1) % GCOLS) == 0 || j == ncols - 1)
+                    if (lane == 31) st_release_cta(&prog[warp + 1], j + 1);
             } else if (to_global) {
-                if (lane == 31) {
-                    grow_out[j] = zbot;
-                    gmrow_out[j] = mbot;
-                }
                 if (((j + 1) & (args.chg - 1)) == 0 || j == ncols - 1)
                     if (lane == 31) st_release_gpu(args.gprog + b, gbase_out + j + 1);
             }
         };
-        auto load_col = [&](int64_t j, R (&vb)[D]) {
-            const int slot = (int)(j & (RING_COLS - 1));
+        // Lane 31's bottom row at column j -> next warp / next stripe.
+        auto bottom_output = [&](int j, Z zb, R mb) {
+            if (to_ring) {
+                if (lane == 31) {
+                    zring[warp + 1][j % ZRS] = zb;
+                    mring[warp + 1][j % ZRS] = mb;
+                }
+            } else if (to_global) {
+                if (lane == 31) {
+                    grow_out[j] = zb;
+                    gmrow_out[j] = mb;
+                }
+            }
+            publish(j);
+        };
+        auto load_col = [&](int j, R (&vb)[D]) {
+            const int slot = j & (NC - 1);
 #pragma unroll
             for (int k = 0; k < D; ++k) vb[k] = ring.v[slot * D + k];
         };
 
-        Z zbot = INF;
-        R mbot = R(0);
-        // Generic step (pipeline fill / drain): lanes outside [0, ncols) idle.
-        auto generic = [&](int64_t st) {
+        Z zbot[C];
+        R mbot[C];
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            zbot[c] = INF;
+            mbot[c] = R(0);
+        }
+        // Generic step (pipeline fill / drain, NaN-exact mode): lanes' columns
+        // outside [0, ncols) idle.
+        auto generic = [&](int st) {
             preamble(st);
-            Z zup = __shfl_up_sync(FULL, zbot, 1);
-            R mup = __shfl_up_sync(FULL, mbot, 1);
-            const int64_t j = st - lane;
-            Z zpn = zup;
-            if (st < ncols) top_input(st, zup, mup, zpn);
-            if (j >= 0 && j < ncols) {
-                R vb[D];
-                load_col(j, vb);
-                const int slot = (int)(j & (RING_COLS - 1));
-                zbot = L.step(vb, ring.t[slot], ring.del[slot], zup, mup, j == 0, args.nu, args.p,
-                              mbot, zpn);
-                if (owner && j == ncols - 1) args.out[0] = L.z_at(own_q);
+            Z zin[C];
+            R min_[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                zin[c] = __shfl_up_sync(FULL, zbot[c], 1);
+                min_[c] = __shfl_up_sync(FULL, mbot[c], 1);
             }
-            if (st >= 31 && st - 31 < ncols) bottom_output(st, zbot, mbot);
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const int j = C * (st - lane) + c;
+                Z zup = zin[c];
+                R mup = min_[c];
+                Z zpn = zup;
+                if (C * st + c < ncols) top_input(st, c, zup, mup, zpn);
+                if (j >= 0 && j < ncols) {
+                    R vb[D];
+                    load_col(j, vb);
+                    const int slot = j & (NC - 1);
+                    zbot[c] = L.step(vb, ring.t[slot], ring.del[slot], zup, mup, j == 0, args.nu,
+                                     args.p, mbot[c], zpn);
+                    if (owner && j == ncols - 1) args.out[0] = L.z_at(own_q);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                const int j = C * (st - 31) + c;
+                if (j >= 0 && j < ncols) bottom_output(j, zbot[c], mbot[c]);
+            }
         };
 
-        const int64_t nsteps = ncols + 31;
-        int64_t st = 0;
-        for (; st < min((int64_t)31, nsteps); ++st) generic(st);
-        // Steady state (safe modes), software-pipelined: chain2 of column j and
-        // the distances + prep of column j+1 form one basic block. Groups of
-        // CHS steps in which every lane is busy run a branch-free body with flow
-        // control once per group; the drain runs the same step lane-predicated.
-        for (; st < min((int64_t)32, nsteps); ++st) generic(st);
+        int st = 0;
+        for (; st < min(32, nsteps); ++st) generic(st);
+        // Steady state (safe modes), software-pipelined: chain2 of a column and
+        // the distances + prep of the next column form one basic block, C times
+        // per step. Groups of CHS steps in which every lane's every column is
+        // valid run a branch-free body with flow control once per group; the
+        // drain runs the same body lane-predicated.
         if (!EXACT_NAN && st < nsteps) {
-            if (warp == 0 && top_boundary) {  // row 0 for st >= 32: z = +inf, d = 0
+            if (warp == 0 && top_boundary) {  // row 0 for columns >= 32C: z = +inf, d = 0
                 for (int c = lane; c < ZRS; c += 32) {
                     gstage[c] = INF;
                     gmstage[c] = R(0);
@@ -589,72 +631,79 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             Z pre[K];
             R tbj;
             {
-                const int j = (int)st - lane;
+                const int j = C * (st - lane);
                 R vb[D];
                 load_col(j, vb);
-                const int slot = j & (RING_COLS - 1);
+                const int slot = j & (NC - 1);
                 R mn[K];
                 L.dists_safe(vb, args.p, mn);
                 tbj = ring.t[slot];
                 L.prep(mn, tbj, ring.del[slot], L.zupp, L.mupp, L.tbp, args.nu, pre);
             }
-            auto body = [&](int t, bool check) {  // check = false: all lanes busy
-                Z zup = __shfl_up_sync(FULL, zbot, 1);
-                R mup = __shfl_up_sync(FULL, mbot, 1);
-                const Z zt = tz[t % ZRS];
-                const R mt = tm[t % ZRS];
-                zup = lane == 0 ? zt : zup;
-                mup = lane == 0 ? mt : mup;
-                const int j = t - lane;
-                if (!check || j < ncols) {
-                    zbot = L.chain2(pre, zup);
-                    mbot = L.mr[K - 1];
-                    if (check && owner && j == ncols - 1) args.out[0] = L.z_at(own_q);
-                    R vb[D];
-                    load_col(j + 1, vb);
-                    const int slot = (j + 1) & (RING_COLS - 1);
-                    R mn[K];
-                    L.dists_safe(vb, args.p, mn);
-                    const R tbn = ring.t[slot];
-                    L.prep(mn, tbn, ring.del[slot], zup, mup, tbj, args.nu, pre);
-                    tbj = tbn;
+            auto body = [&](int t, bool check) {  // check = false: every column valid
+                Z zin[C];
+                R min_[C];
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    zin[c] = __shfl_up_sync(FULL, zbot[c], 1);
+                    min_[c] = __shfl_up_sync(FULL, mbot[c], 1);
+                    const Z zt = tz[(C * t + c) % ZRS];
+                    const R mt = tm[(C * t + c) % ZRS];
+                    zin[c] = lane == 0 ? zt : zin[c];
+                    min_[c] = lane == 0 ? mt : min_[c];
                 }
-                if (ow && (!check || t - 31 < ncols)) {
-                    oz[(t - 31) & omask] = zbot;
-                    om[(t - 31) & omask] = mbot;
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const int j = C * (t - lane) + c;  // column j + 1 next
+                    if (!check || j < ncols) {
+                        zbot[c] = L.chain2(pre, zin[c]);
+                        mbot[c] = L.mr[K - 1];
+                        if (check && owner && j == ncols - 1) args.out[0] = L.z_at(own_q);
+                        R vb[D];
+                        load_col(j + 1, vb);
+                        const int slot = (j + 1) & (NC - 1);
+                        R mn[K];
+                        L.dists_safe(vb, args.p, mn);
+                        const R tbn = ring.t[slot];
+                        L.prep(mn, tbn, ring.del[slot], zin[c], min_[c], tbj, args.nu, pre);
+                        tbj = tbn;
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const int j = C * (t - 31) + c;
+                    if (ow && (!check || j < ncols)) {
+                        oz[j & omask] = zbot[c];
+                        om[j & omask] = mbot[c];
+                    }
                 }
             };
-            // full groups: every step t of the group has all lanes in [0, ncols - 1)
-            while (st + CHS < ncols) {
-                const int st0 = (int)st;
+            // full groups: lane 0's last column in the group is < ncols - 1
+            while (C * (st + CHS) < ncols) {
+                const int st0 = st;
                 preamble(st);
-                if (to_ring) {  // lane 31 writes columns <= st0 - 16 this group
-                    const int need = st0 - 16 - ZRS + 1;
+                if (to_ring) {  // lane 31 writes columns < C*(st0 - 15) this group
+                    const int need = C * (st0 - 15) - ZRS;
                     while (ld_acquire_cta(&cons[warp + 1]) < need) spin_pause();
                 }
 #pragma unroll WAVE_UNROLL
                 for (int i = 0; i < CHS; ++i) body(st0 + i, false);
                 st += CHS;
-                const int done = (int)st - 31;  // lane 31 finished columns [0, done)
+                const int done = C * (st - 31);  // lane 31 finished columns [0, done)
                 if (to_ring) {
                     if (lane == 31) st_release_cta(&prog[warp + 1], done);
-                } else if (to_global && ((done & (args.chg - 1)) < CHS)) {
+                } else if (to_global && ((done & (args.chg - 1)) < GCOLS)) {
                     if (lane == 31) st_release_gpu(args.gprog + b, gbase_out + done);
                 }
             }
-            // drain: per-step flow control, lanes predicated on their column
+            // drain: per-step flow control, lanes predicated on their columns
             for (; st < nsteps; ++st) {
                 preamble(st);
-                body((int)st, true);
-                const int64_t j31 = st - 31;
-                if (j31 >= 0 && j31 < ncols) {
-                    if (to_ring) {
-                        if (((j31 + 1) % CHS) == 0 || j31 == ncols - 1)
-                            if (lane == 31) st_release_cta(&prog[warp + 1], (int)(j31 + 1));
-                    } else if (to_global) {
-                        if (((j31 + 1) & (args.chg - 1)) == 0 || j31 == ncols - 1)
-                            if (lane == 31) st_release_gpu(args.gprog + b, gbase_out + j31 + 1);
-                    }
+                body(st, true);
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    const int j = C * (st - 31) + c;
+                    if (j >= 0 && j < ncols) publish(j);
                 }
             }
         }

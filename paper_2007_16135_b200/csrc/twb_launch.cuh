@@ -88,14 +88,14 @@ cudaError_t run_batch(BatchArgs<R, Z> a, int64_t max_rows, cudaStream_t st, Laun
 
 // Wavefront variants (rows per lane K, warps per CTA W, CTAs per SM MINB);
 // run_wave picks one by the row-side length.
-template <int D, int K, int P, bool E, bool N1, int W, int MINB, typename R, typename Z>
+template <int D, int K, int C, int P, bool E, bool N1, int W, int MINB, typename R, typename Z>
 cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream_t st,
                          LaunchCtx* ctx) {
-    auto kern = wave_kernel<D, K, P, E, N1, W, MINB, R, Z>;
+    auto kern = wave_kernel<D, K, C, P, E, N1, W, MINB, R, Z>;
     int sms = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t smem = wave_smem<D, R, Z>(W);
+    const size_t smem = wave_smem<D, R, Z, C>(W);
     int occ = 0;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -180,14 +180,16 @@ cudaError_t run_wave(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // TWB_WAVE_CFG pins a variant (tuning experiments; proven-safe modes):
-    // k<rows per lane>w<warps per CTA>
+    // k<rows per lane>w<warps per CTA>[c<columns per step>]
     if constexpr (!E) {
         if (const char* env = getenv("TWB_WAVE_CFG")) {
             const std::string c(env);
-            if (c == "k8w8") return run_wave_cfg<D, 8, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k6w12") return run_wave_cfg<D, 6, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k4w12") return run_wave_cfg<D, 4, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k2w8") return run_wave_cfg<D, 2, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k8w8") return run_wave_cfg<D, 8, 1, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k6w12") return run_wave_cfg<D, 6, 1, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k4w12") return run_wave_cfg<D, 4, 1, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k6w12c2") return run_wave_cfg<D, 6, 2, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k4w12c2") return run_wave_cfg<D, 4, 2, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k8w8c2") return run_wave_cfg<D, 8, 2, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
         }
     }
     // Long row side (>= 1.5 rounds of stripes): 12 warps x 6 rows per lane
@@ -196,8 +198,8 @@ cudaError_t run_wave(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream
     // Shorter: 4 rows per lane, stripes of up to 12 warps sized by the cost
     // model (n = 300k d = 3: 346 GCUPS; n = 100k: d = 1 331, d = 3 170).
     if (pr.nA >= (int64_t)sms * 12 * 32 * 6 * 3 / 2)
-        return run_wave_cfg<D, 6, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
-    return run_wave_cfg<D, 4, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
+        return run_wave_cfg<D, 6, 1, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
+    return run_wave_cfg<D, 4, 1, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
 }
 
 }  // namespace twb

@@ -39,11 +39,13 @@ struct PreparedT {
 
 constexpr int RING_COLS = 128;  // per-warp column staging ring (4 blocks of 32)
 
-template <int D, typename R, typename Z>
+// Per-warp column staging ring of NC columns (power of 2, multiple of 32).
+template <int D, typename R, typename Z, int NC = RING_COLS>
 struct ColRing {
-    R v[RING_COLS * D];
-    R t[RING_COLS];
-    Z del[RING_COLS];
+    static constexpr int N = NC;
+    R v[NC * D];
+    R t[NC];
+    Z del[NC];
 };
 
 template <typename X>
@@ -54,14 +56,14 @@ __device__ __forceinline__ void cp_async_elem(X* smem, const X* gmem, bool valid
 
 // Stage 32-column block `blk` (stream columns 32*blk .. 32*blk+31, i.e. global
 // prepared rows c0 + ...) into its ring slot. Columns >= ncols are zero-filled.
-template <int D, typename R, typename Z>
-__device__ __forceinline__ void stage_block(ColRing<D, R, Z>& ring, const PreparedT<R, Z>& B,
+template <int D, typename R, typename Z, int NC>
+__device__ __forceinline__ void stage_block(ColRing<D, R, Z, NC>& ring, const PreparedT<R, Z>& B,
                                             int64_t c0, int64_t ncols, int64_t blk, int lane) {
     const int64_t j = blk * 32 + lane;
     const bool ok = j < ncols;
     const int64_t g = c0 + (ok ? j : 0);
-    const int slot = (int)(j & (RING_COLS - 1));
-    const int base = (int)((blk * 32) & (RING_COLS - 1)) * D;
+    const int slot = (int)(j & (NC - 1));
+    const int base = (int)((blk * 32) & (NC - 1)) * D;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
         const int e = lane + 32 * k;  // element of the block's 32*D words
