@@ -376,6 +376,7 @@ def run_ours(args, world, rank, local):
     batch = None
     if not args.no_batch:
         batch = run_batch_cfg5(args, world, rank, local)
+    extra = {} if args.no_extra else run_extra(args, world, rank, local)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -408,8 +409,61 @@ def run_ours(args, world, rank, local):
             "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
             "clocks": clocks.summary(), "gpu_launches": launches,
             "batch": batch,
+            "other_configs": extra,
         }
         print(json.dumps(line), flush=True)
+
+
+def run_extra(args, world, rank, local):
+    """The other BASELINE configs, kernel-timed on this rank (events inside
+    libtwb200, device-resident inputs): cfg3 in fp32 mode, cfg2, cfg1, and the
+    cfg4 full 1000 x 1000 fp64 matrix sharded by rows over the ranks."""
+    import torch
+
+    import paper_2007_16135_b200 as twb
+    from paper_2007_16135_b200 import _lib
+    from paper_2007_16135_b200.distributed import row_bounds
+    from paper_2007_16135_b200.workloads import make_pair, make_set
+
+    lib = _lib.load()
+    lib.twb_set_kernel_timing(1)
+    dev = torch.device("cuda", local)
+    res = {}
+    for name in ("cfg3_f32", "cfg2", "cfg1"):
+        wl = WORKLOADS[name]
+        dt = np.float32 if wl["dtype"] == "f32" else np.float64
+        a, ta, b, tb = (torch.from_numpy(np.ascontiguousarray(x.astype(dt))).to(dev)
+                        for x in make_pair(wl["n"], wl["d"], wl["seed"]))
+        out = twb.twed_dev(a, ta, b, tb, nu=1.0, lamb=1.0, degree=2)
+        torch.cuda.synchronize()
+        ks = []
+        reps = 2 if wl["n"] >= 1_000_000 else 5
+        for _ in range(reps):
+            twb.twed_dev(a, ta, b, tb, nu=1.0, lamb=1.0, degree=2, out=out)
+            ks.append(lib.twb_last_kernel_ms())
+        kms = max_over_ranks(float(np.median(ks)), world)
+        res[name] = {"n": wl["n"], "d": wl["d"], "dtype": wl["dtype"], "kernel_ms": kms,
+                     "gcups": wl["n"] * wl["n"] / (kms * 1e-3) / 1e9, "result": out.item()}
+    # cfg4: AA 1000 x 256 (seed 3) against BB 1000 x 256 (seed 4), d = 1, fp64, full
+    AA, TAA = make_set(1000, 256, 1, 3)
+    BB, TBB = make_set(1000, 256, 1, 4)
+    dA = torch.from_numpy(AA.reshape(-1, 1)).to(dev)
+    dTA = torch.from_numpy(TAA.reshape(-1)).to(dev)
+    dB = torch.from_numpy(BB.reshape(-1, 1)).to(dev)
+    dTB = torch.from_numpy(TBB.reshape(-1)).to(dev)
+    off = np.arange(1001, dtype=np.int64) * 256
+    b0, b1 = row_bounds(1000, world, False)[rank]
+    R = torch.empty((b1 - b0, 1000), dtype=torch.float64, device=dev)
+    ks = []
+    for _ in range(4):
+        twb.twed_batch_dev(dA, off, dTA, dB, off, dTB, nu=1.0, lamb=1.0, degree=2, tri=False,
+                           row_begin=b0, row_end=b1, out=R)
+        ks.append(lib.twb_last_kernel_ms())
+    kms = max_over_ranks(float(np.median(ks[1:])), world)
+    res["cfg4"] = {"pairs": 1_000_000, "kernel_ms": kms, "pairs_per_s": 1e6 / (kms * 1e-3),
+                   "gcups": 1e6 * 256 * 256 / (kms * 1e-3) / 1e9, "n_gpus": world,
+                   "sharding": "rows, no collective in the timed kernel"}
+    return res
 
 
 def run_batch_cfg5(args, world, rank, local):
@@ -490,6 +544,7 @@ def main():
     ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-batch", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true")
     ap.add_argument("--batch-n", type=int, default=10_000)
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--ref-step-s", type=float, default=8.0)
