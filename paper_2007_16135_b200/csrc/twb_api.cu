@@ -84,6 +84,15 @@ void init_pool(int dev) {
     });
 }
 
+// Device-resident entry points run on the caller's current device. Without
+// this, the default pool's release threshold (0) hands the 1M pair's boundary
+// rows back to the driver at every synchronisation and the next call re-maps
+// them (12 ms per call, spikes of 150-250 ms on the B200).
+void init_pool_current() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) init_pool(dev);
+}
+
 // ---------------------------------------------------------------------------
 // "safe" inputs: every value/time finite with |x| < 2^500 (fp64) or 2^60
 // (fp32), nu and lam finite and small. Then no cell candidate can be NaN or
@@ -239,6 +248,7 @@ constexpr double safe_tiny() {
 template <typename T, typename R, typename Z>
 int twed_pair_dev(const T* dA, int64_t nA, const T* dTA, const T* dB, int64_t nB, const T* dTB,
                   int dim, double nu, double lam, int degree, cudaStream_t st, double* d_out) {
+    init_pool_current();
     Scratch sc(st);
     int* dflag = sc.get_n<int>(1);
     if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
@@ -535,6 +545,7 @@ int twed_batch_dev(const T* dAA, const int64_t* a_off, int64_t nAA, const T* dTA
                          row_end);
     if (rc) return rc;
     if (tri && !self) return fail(TWB_EINVAL, "symmetric=True requires both lists to be the same collection");
+    init_pool_current();
     if constexpr (sizeof(T) == 8) {
         return twed_batch_dev_impl<T, double, double, O>(dAA, a_off, nAA, dTAA, dBB, b_off, nBB,
                                                          dTBB, dim, nu, lam, degree, tri, row_begin,

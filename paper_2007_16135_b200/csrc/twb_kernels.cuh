@@ -347,6 +347,11 @@ __device__ __forceinline__ void spin_pause() {
 #define TWB_WAVE_UNROLL 2
 #endif
 constexpr int WAVE_UNROLL = TWB_WAVE_UNROLL;
+// Timing experiments only (results are wrong): 1 = CTAs do not wait for the
+// previous stripe's boundary row, 2 = warps do not wait for each other either.
+#ifndef TWB_DBG_NOSYNC
+#define TWB_DBG_NOSYNC 0
+#endif
 constexpr int ZRS = 256;  // shared-memory ring between consecutive warps (columns)
 constexpr int CHS = 16;   // warp-to-warp publish granularity (columns)
 constexpr int CHG = 32;   // CTA-to-CTA read granularity (columns; publish = args.chg)
@@ -458,7 +463,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         R pm[C];
         auto fetch = [&](int c0) {  // columns [c0, c0 + 32C) -> registers
             const long long need = gbase_in + min(c0 + 32 * C, ncols);
-            while (ld_acquire_gpu(args.gprog + pb) < need) __nanosleep(32);
+            if (TWB_DBG_NOSYNC < 1) gwait(args.gprog + pb, need);
 #pragma unroll
             for (int k = 0; k < C; ++k) {
                 const int c = c0 + 32 * k + lane;
@@ -493,12 +498,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             if (warp > 0 && (st % CHS) == 0 && C * st < ncols) {
                 if (lane == 0) st_release_cta(&cons[warp], C * st);
                 const int need = min(C * (st + CHS), ncols);
-                while (ld_acquire_cta(&prog[warp]) < need) spin_pause();
+                while (TWB_DBG_NOSYNC < 2 && ld_acquire_cta(&prog[warp]) < need) spin_pause();
             }
             const int j31 = C * (st - 31);  // lane 31's first column this step
             if (to_ring && j31 >= 0 && j31 < ncols && (j31 % GCOLS) == 0) {
                 const int need = j31 + GCOLS - ZRS;
-                while (ld_acquire_cta(&cons[warp + 1]) < need) spin_pause();
+                while (TWB_DBG_NOSYNC < 2 && ld_acquire_cta(&cons[warp + 1]) < need) spin_pause();
             }
         };
         // The row above lane 0 at column C*st + c, read by every lane from a
@@ -672,10 +677,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
                     const int j = C * (t - 31) + c;
-                    if (ow && (!check || j < ncols)) {
-                        oz[j & omask] = zbot[c];
-                        om[j & omask] = mbot[c];
-                    }
+                    // predicated, not branched: a lane-31-only branch makes
+                    // every step a divergent region (BSSY/BSYNC + branch stalls)
+                    const bool w = ow && (!check || j < ncols);
+                    st_pred(oz + (j & omask), zbot[c], w);
+                    st_pred(om + (j & omask), mbot[c], w);
                 }
             };
             // full groups: lane 0's last column in the group is < ncols - 1
@@ -684,7 +690,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                 preamble(st);
                 if (to_ring) {  // lane 31 writes columns < C*(st0 - 15) this group
                     const int need = C * (st0 - 15) - ZRS;
-                    while (ld_acquire_cta(&cons[warp + 1]) < need) spin_pause();
+                    while (TWB_DBG_NOSYNC < 2 && ld_acquire_cta(&cons[warp + 1]) < need) spin_pause();
                 }
 #pragma unroll WAVE_UNROLL
                 for (int i = 0; i < CHS; ++i) body(st0 + i, false);
