@@ -659,6 +659,16 @@ __global__ void sqrt_check_kernel(int64_t n, unsigned long long seed, unsigned l
             ++nf;
             nb += __double_as_longlong(sqrt_fast(x)) != __double_as_longlong(__dsqrt_rn(x));
         }
+        // the K-wide form on the safe-mode domain {0} U [2^-904, 2^1004)
+        // (twb_device.cuh sqrt_fast0_k), zero included in every vector
+        const unsigned hx = (unsigned)(bits >> 32);
+        const double xs = (hx >= 0x07700000u && hx < 0x7eb00000u) ? x : 1.0 + (double)(i & 1023);
+        const double v[4] = {xs, 0.0, __dmul_rn(xs, 0.25), __dadd_rn(xs, 1.0)};
+        double o[4];
+        sqrt_fast0_k<4>(v, o);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            nb += __double_as_longlong(o[q]) != __double_as_longlong(__dsqrt_rn(v[q]));
     }
     atomicAdd(bad, nb);
     atomicAdd(fast, nf);
