@@ -364,10 +364,30 @@ __host__ __device__ constexpr size_t wave_smem_rings(int warps) {
     return (sizeof(WaveRing<D, R, Z, C>) * warps + 15) / 16 * 16;
 }
 // rings | zring[W][ZRS] | mring[W][ZRS] | gstage z[ZRS] | gstage m[ZRS] | prog[W] | cons[W]
+// TWB_WAVE_SA: the lanes' rows of A in shared memory (LaneRows SA) instead
+// of registers.
+// -1 (default): fp64 with d >= 2, where the 3*K registers of row values
+// crowd the scheduler (B200, n = 1M, d = 3: 468 vs 438 GCUPS); with d = 1 the
+// extra LDS cost more than they free (944 vs 1015).
+#ifndef TWB_WAVE_SA
+#define TWB_WAVE_SA -1
+#endif
+template <int D, typename R>
+__host__ __device__ constexpr bool wave_sa() {
+    return TWB_WAVE_SA < 0 ? (D >= 2 && sizeof(R) == 8) : TWB_WAVE_SA != 0;
+}
+template <int D, typename R, int K>
+__host__ __device__ constexpr size_t wave_smem_rows(int warps) {
+    return wave_sa<D, R>() ? (size_t)warps * 32 * K * RowChunks<D, R>::BYTES_PER_LANE_ROW : 0;
+}
 template <int D, typename R, typename Z, int C>
+__host__ __device__ constexpr size_t wave_smem_base(int warps) {  // 16-aligned
+    return (wave_smem_rings<D, R, Z, C>(warps) + sizeof(Z) * (ZRS * warps + ZRS) +
+            sizeof(R) * (ZRS * warps + ZRS) + sizeof(int) * 2 * warps + 15) / 16 * 16;
+}
+template <int D, typename R, typename Z, int C, int K>
 __host__ __device__ constexpr size_t wave_smem(int warps) {
-    return wave_smem_rings<D, R, Z, C>(warps) + sizeof(Z) * (ZRS * warps + ZRS) +
-           sizeof(R) * (ZRS * warps + ZRS) + sizeof(int) * 2 * warps;
+    return wave_smem_base<D, R, Z, C>(warps) + wave_smem_rows<D, R, K>(warps);
 }
 
 template <typename R, typename Z>
@@ -392,7 +412,7 @@ struct WaveArgs {
 template <int D, int K, int C, int P, bool EXACT_NAN, bool NU1, int WARPS, int MINB, typename R,
           typename Z>
 __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R, Z> args) {
-    using Lane = LaneRows<D, K, P, EXACT_NAN, NU1, R, Z>;
+    using Lane = LaneRows<D, K, P, EXACT_NAN, NU1, R, Z, wave_sa<D, R>()>;
     using Ring = WaveRing<D, R, Z, C>;
     constexpr int NC = Ring::N;
     constexpr int GCOLS = C * CHS;  // columns per group of CHS steps
@@ -409,6 +429,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
     p0 += sizeof(R) * ZRS;
     int* prog = reinterpret_cast<int*>(p0);
     int* cons = prog + WARPS;
+    R* srows = reinterpret_cast<R*>(smem_raw + wave_smem_base<D, R, Z, C>(WARPS));  // SA rows (16-aligned)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int G = gridDim.x;
@@ -419,6 +440,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
     const int ncols = (int)(args.nB + 1);
     const int nsteps = (ncols + C - 1) / C + 31;
     Lane L;
+    if constexpr (wave_sa<D, R>())
+        L.sa = srows + ((size_t)warp * K * Lane::RC::NCH * 32 + lane) * Lane::RC::EPC;
 
     const int64_t s_last = (args.nA - 1) / args.H;
     const int64_t loc_last = (args.nA - 1) - s_last * args.H;

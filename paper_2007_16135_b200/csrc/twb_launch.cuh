@@ -95,7 +95,7 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
     int sms = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t smem = wave_smem<D, R, Z, C>(W);
+    const size_t smem = wave_smem<D, R, Z, C, K>(W);
     int occ = 0;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -187,6 +187,12 @@ cudaError_t run_wave(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream
             if (c == "k8w8") return run_wave_cfg<D, 8, 1, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
             if (c == "k6w12") return run_wave_cfg<D, 6, 1, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
             if (c == "k4w12") return run_wave_cfg<D, 4, 1, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
+#ifdef TWB_WAVE_EXTRA_CFGS  // tuning builds only
+            if (c == "k6w16") return run_wave_cfg<D, 6, 1, P, E, N1, 16, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k4w16") return run_wave_cfg<D, 4, 1, P, E, N1, 16, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k8w12") return run_wave_cfg<D, 8, 1, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
+            if (c == "k5w16") return run_wave_cfg<D, 5, 1, P, E, N1, 16, 1, R, Z>(pr, alloc, st, ctx);
+#endif
             // C = 2 (two columns per lane step) measured within 3% of C = 1
             // on the B200 (profiles/r01_c2_variants.log): not instantiated.
         }

@@ -173,13 +173,60 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 // The work of one column is split in two so kernels can software-pipeline it:
 // dists() (the K local distances, independent of the wavefront) and chain()
 // (the K-row min recurrence that carries z down the lane's rows).
-template <int D, int K, int P, bool EXACT_NAN, bool NU1, typename R, typename Z>
+// SA (shared-memory rows): the lane's K rows of A (values and times) live in
+// shared memory instead of registers, [row][16-byte chunk][32 lanes] so every
+// warp-wide LDS.128 is one contiguous 512-byte access; frees (D+1)*K*2
+// registers per thread for the scheduler. sa = this lane's first chunk.
+template <int D, typename R>
+struct RowChunks {
+    static constexpr int EPC = 16 / sizeof(R);                // elements per chunk
+    static constexpr int NCH = (D + 1 + EPC - 1) / EPC;       // chunks per row
+    static constexpr int BYTES_PER_LANE_ROW = NCH * 16;
+};
+
+template <int D, int K, int P, bool EXACT_NAN, bool NU1, typename R, typename Z, bool SA = false>
 struct LaneRows {
     static constexpr bool F32 = sizeof(R) == 4;
     static constexpr bool SPLIT_SQRT = !F32 && D >= 2 && P == 2;
     static constexpr bool COL0_BY_INF = !EXACT_NAN;
-    R a[K][D];
-    R ta[K];
+    using RC = RowChunks<D, R>;
+    R a[SA ? 1 : K][D];
+    R ta[SA ? 1 : K];
+    R* sa = nullptr;  // SA: element (lane * EPC) of the warp's row block
+
+    // values and time of row slot q
+    __device__ __forceinline__ void row(int q, R (&v)[D], R& t) const {
+        if constexpr (SA) {
+            R e[RC::NCH * RC::EPC];
+#pragma unroll
+            for (int c = 0; c < RC::NCH; ++c) {
+                const R* src = sa + (q * RC::NCH + c) * 32 * RC::EPC;
+                if constexpr (sizeof(R) == 8) {
+                    const double2 w = *reinterpret_cast<const double2*>(src);
+                    e[2 * c] = w.x;
+                    e[2 * c + 1] = w.y;
+                } else {
+                    const float4 w = *reinterpret_cast<const float4*>(src);
+                    e[4 * c] = w.x;
+                    e[4 * c + 1] = w.y;
+                    e[4 * c + 2] = w.z;
+                    e[4 * c + 3] = w.w;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < D; ++k) v[k] = e[k];
+            t = e[D];
+        } else {
+#pragma unroll
+            for (int k = 0; k < D; ++k) v[k] = a[q][k];
+            t = ta[q];
+        }
+    }
+    __device__ __forceinline__ R row_t(int q) const {
+        R v[D], t;
+        row(q, v, t);
+        return t;
+    }
     Z da[K];
     Z zl[K];  // z(r, j-1)
     R mr[K];  // fp64: d(r, j-1); fp32: c(r, j-1)
@@ -198,9 +245,23 @@ struct LaneRows {
             const int64_t r = r0 + q;
             const bool ok = r <= n;
             const int64_t g = base + (ok ? r : 0);
+            if constexpr (SA) {
+                R e[RC::NCH * RC::EPC];
 #pragma unroll
-            for (int k = 0; k < D; ++k) a[q][k] = ok ? A.v[g * D + k] : R(0);
-            ta[q] = ok ? A.t[g] : R(0);
+                for (int k = 0; k < RC::NCH * RC::EPC; ++k) e[k] = R(0);
+#pragma unroll
+                for (int k = 0; k < D; ++k) e[k] = ok ? A.v[g * D + k] : R(0);
+                e[D] = ok ? A.t[g] : R(0);
+#pragma unroll
+                for (int c = 0; c < RC::NCH; ++c)
+#pragma unroll
+                    for (int k = 0; k < RC::EPC; ++k)
+                        sa[(q * RC::NCH + c) * 32 * RC::EPC + k] = e[c * RC::EPC + k];
+            } else {
+#pragma unroll
+                for (int k = 0; k < D; ++k) a[q][k] = ok ? A.v[g * D + k] : R(0);
+                ta[q] = ok ? A.t[g] : R(0);
+            }
             da[q] = ok ? A.del[g] : Z(0);
         }
         const int64_t ru = r0 - 1;
@@ -222,32 +283,42 @@ struct LaneRows {
             bool ok = true;
 #pragma unroll
             for (int q = 0; q < K; ++q) {
-                const double acc = sumsq<D>(a[q], vb);
+                R av[D], t;
+                row(q, av, t);
+                const double acc = sumsq<D>(av, vb);
                 ok &= sqrt_fast_ok(acc);
                 mn[q] = sqrt_fast(acc);
             }
             if (!ok) {
 #pragma unroll
                 for (int q = 0; q < K; ++q) {
-                    const double acc = sumsq<D>(a[q], vb);
+                    R av[D], t;
+                    row(q, av, t);
+                    const double acc = sumsq<D>(av, vb);
                     if (!sqrt_fast_ok(acc)) mn[q] = __dsqrt_rn(acc);
                 }
             }
         } else if constexpr (F32 && D >= 2 && P == 2) {
 #pragma unroll
             for (int q = 0; q < K; ++q) {
-                const float d0 = a[q][0] - vb[0];
+                R av[D], t;
+                row(q, av, t);
+                const float d0 = av[0] - vb[0];
                 float acc = d0 * d0;
 #pragma unroll
                 for (int k = 1; k < D; ++k) {
-                    const float dk = a[q][k] - vb[k];
+                    const float dk = av[k] - vb[k];
                     acc = __fmaf_rn(dk, dk, acc);
                 }
                 mn[q] = sqrt_approx<!EXACT_NAN>(acc);
             }
         } else {
 #pragma unroll
-            for (int q = 0; q < K; ++q) mn[q] = dist<D, P, R>(a[q], vb, p);
+            for (int q = 0; q < K; ++q) {
+                R av[D], t;
+                row(q, av, t);
+                mn[q] = dist<D, P, R>(av, vb, p);
+            }
         }
     }
 
@@ -265,7 +336,7 @@ struct LaneRows {
             R c_up = mupp;
 #pragma unroll
             for (int q = 0; q < K; ++q) {
-                const float g = ta[q] - tb;
+                const float g = row_t(q) - tb;
                 const float c = NU1 ? mn[q] + fabsf(g) : __fmaf_rn(nuf, fabsf(g), mn[q]);
                 const float w = c + c_up;
                 Z match;
@@ -287,7 +358,7 @@ struct LaneRows {
 #pragma unroll
             for (int q = 0; q < K; ++q) {
                 const R m = mn[q];
-                const R g = ta[q] - tb;
+                const R g = row_t(q) - tb;
                 // ((z_diag + d_now) + d_prev) + nu * (|g_now| + |g_prev|)
                 const double gs = __dadd_rn(fabs(g), fabs(g_up));
                 const double tt = NU1 ? gs : __dmul_rn(nu, gs);
@@ -327,7 +398,11 @@ struct LaneRows {
         if constexpr (SPLIT_SQRT) {
             double acc[K];
 #pragma unroll
-            for (int q = 0; q < K; ++q) acc[q] = sumsq<D>(a[q], vb);
+            for (int q = 0; q < K; ++q) {
+                R av[D], t;
+                row(q, av, t);
+                acc[q] = sumsq<D>(av, vb);
+            }
             sqrt_fast0_k<K>(acc, mn);
         } else {
             dists(vb, p, mn);
@@ -343,7 +418,7 @@ struct LaneRows {
             const float nuf = (float)nu;
 #pragma unroll
             for (int q = K - 1; q >= 0; --q) {
-                const float g = ta[q] - tb;
+                const float g = row_t(q) - tb;
                 const float c = NU1 ? mn[q] + fabsf(g) : __fmaf_rn(nuf, fabsf(g), mn[q]);
                 const float c_up = q > 0 ? mr[q - 1] : m0;
                 const Z zd = q > 0 ? zl[q - 1] : zd0;
@@ -359,7 +434,7 @@ struct LaneRows {
         } else {
 #pragma unroll
             for (int q = K - 1; q >= 0; --q) {
-                const R g = ta[q] - tb;
+                const R g = row_t(q) - tb;
                 const R g_up = q > 0 ? gr[q - 1] : tup - tbprev;
                 const R m_up = q > 0 ? mr[q - 1] : m0;
                 const Z zd = q > 0 ? zl[q - 1] : zd0;
