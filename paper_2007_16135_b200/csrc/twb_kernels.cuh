@@ -355,6 +355,7 @@ constexpr int WAVE_UNROLL = TWB_WAVE_UNROLL;
 constexpr int ZRS = 256;  // shared-memory ring between consecutive warps (columns)
 constexpr int CHS = 16;   // warp-to-warp publish granularity (columns)
 constexpr int CHG = 32;   // CTA-to-CTA read granularity (columns; publish = args.chg)
+constexpr int CHG_RAMP = 4096;  // publish every group for the first columns of a stripe
 
 template <int D, typename R, typename Z, int C>
 using WaveRing = ColRing<D, R, Z, RING_COLS * C>;
@@ -403,7 +404,14 @@ struct WaveArgs {
     double nu;
     int p;
     double* out;
+    long long* dbg;  // diagnostics (TWB_DBG_TIMES): per stripe start / input ready / end (ns)
 };
+
+__device__ __forceinline__ long long globaltimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // Stripe sweep. C = columns per lane step: lane t at step s handles columns
 // C*(s - t) + c, c < C, so one step carries C*K cells per lane and the
@@ -461,6 +469,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         const int wact = (int)((rows + 32 * K - 1) / (32 * K));
         if (warp >= wact) continue;
 
+        if (args.dbg && lane == 0) {
+            if (warp == 0) args.dbg[s * 4] = globaltimer();
+            args.dbg[args.S * (4 + WARPS) + s * WARPS + warp] = globaltimer();
+        }
         L.load(args.A, 0, first_row + (int64_t)(warp * 32 + lane) * K, args.nA);
         // columns [0, 64C): the first 64 steps
 #pragma unroll
@@ -495,6 +507,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             }
         };
         if (from_global) fetch(0);
+        if (args.dbg && warp == 0 && lane == 0) args.dbg[s * 4 + 1] = globaltimer();
 
         // Warp-uniform per-step bookkeeping: column staging, boundary-row
         // fetch, ring flow control with the neighbouring warps.
@@ -634,12 +647,24 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         };
 
         int st = 0;
-        for (; st < min(32, nsteps); ++st) generic(st);
+        // Pipeline fill (the first 32 steps, lanes t > st idle): the pipelined
+        // body below, lane-predicated. The fill is on the critical path of the
+        // whole sweep (each warp's lane 31 feeds the next warp, each CTA the
+        // next CTA), and the generic step runs ~2.4x slower than the pipelined
+        // one (B200, n = 1M: 51 vs 21 us per warp). Tiny rows keep the generic
+        // path.
+#ifndef TWB_PFILL
+#define TWB_PFILL 1
+#endif
+        const bool pfill = TWB_PFILL && !EXACT_NAN && ncols > C * (32 + 2 * CHS) + 64;
+        if (!pfill)
+            for (; st < min(32, nsteps); ++st) generic(st);
         // Steady state (safe modes), software-pipelined: chain2 of a column and
         // the distances + prep of the next column form one basic block, C times
         // per step. Groups of CHS steps in which every lane's every column is
         // valid run a branch-free body with flow control once per group; the
         // drain runs the same body lane-predicated.
+        if (args.dbg && lane == 0) args.dbg[args.S * 4 + s * WARPS + warp] = globaltimer();
         if (!EXACT_NAN && st < nsteps) {
             if (warp == 0 && top_boundary) {  // row 0 for columns >= 32C: z = +inf, d = 0
                 for (int c = lane; c < ZRS; c += 32) {
@@ -657,8 +682,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             const int omask = to_ring ? ZRS - 1 : (to_global ? 0x7fffffff : 0);
             const bool ow = lane == 31 && (to_ring || to_global);
             Z pre[K];
-            R tbj;
-            {
+#pragma unroll
+            for (int q = 0; q < K; ++q) pre[q] = INF;
+            R tbj = L.tbp;
+            if (C * (st - lane) >= 0) {
                 const int j = C * (st - lane);
                 R vb[D];
                 load_col(j, vb);
@@ -668,7 +695,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                 tbj = ring.t[slot];
                 L.prep(mn, tbj, ring.del[slot], L.zupp, L.mupp, L.tbp, args.nu, pre);
             }
-            auto body = [&](int t, bool check) {  // check = false: every column valid
+            // check = false: every column < ncols; fill: columns may be < 0
+            // (the lane has not started: no chain, prep only from column 0 on)
+            auto body = [&](int t, bool check, bool fill) {
                 Z zin[C];
                 R min_[C];
 #pragma unroll
@@ -683,7 +712,25 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
                     const int j = C * (t - lane) + c;  // column j + 1 next
-                    if (!check || j < ncols) {
+                    if (fill) {
+                        if (j >= 0) {
+                            zbot[c] = L.chain2(pre, zin[c]);
+                            mbot[c] = L.mr[K - 1];
+                        }
+                        if (j + 1 >= 0) {
+                            // z(0, 0) = 0 is the diagonal of cell (1, 1); the
+                            // row-0 ring holds +inf (the row above column 0)
+                            const Z zd0 = (top_boundary && lane == 0 && j == 0) ? Z(0) : zin[c];
+                            R vb[D];
+                            load_col(j + 1, vb);
+                            const int slot = (j + 1) & (NC - 1);
+                            R mn[K];
+                            L.dists_safe(vb, args.p, mn);
+                            const R tbn = ring.t[slot];
+                            L.prep(mn, tbn, ring.del[slot], zd0, min_[c], tbj, args.nu, pre);
+                            tbj = tbn;
+                        }
+                    } else if (!check || j < ncols) {
                         zbot[c] = L.chain2(pre, zin[c]);
                         mbot[c] = L.mr[K - 1];
                         if (check && owner && j == ncols - 1) args.out[0] = L.z_at(own_q);
@@ -702,7 +749,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                     const int j = C * (t - 31) + c;
                     // predicated, not branched: a lane-31-only branch makes
                     // every step a divergent region (BSSY/BSYNC + branch stalls)
-                    const bool w = ow && (!check || j < ncols);
+                    const bool w = ow && (!check || j < ncols) && (!fill || j >= 0);
                     st_pred(oz + (j & omask), zbot[c], w);
                     st_pred(om + (j & omask), mbot[c], w);
                 }
@@ -715,20 +762,29 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                     const int need = C * (st0 - 15) - ZRS;
                     while (TWB_DBG_NOSYNC < 2 && ld_acquire_cta(&cons[warp + 1]) < need) spin_pause();
                 }
+                if (st0 < 32) {
+                    for (int i = 0; i < CHS; ++i) body(st0 + i, false, true);
+                } else {
 #pragma unroll WAVE_UNROLL
-                for (int i = 0; i < CHS; ++i) body(st0 + i, false);
+                    for (int i = 0; i < CHS; ++i) body(st0 + i, false, false);
+                }
                 st += CHS;
                 const int done = C * (st - 31);  // lane 31 finished columns [0, done)
-                if (to_ring) {
-                    if (lane == 31) st_release_cta(&prog[warp + 1], done);
-                } else if (to_global && ((done & (args.chg - 1)) < GCOLS)) {
-                    if (lane == 31) st_release_gpu(args.gprog + b, gbase_out + done);
+                if (done > 0) {
+                    if (to_ring) {
+                        if (lane == 31) st_release_cta(&prog[warp + 1], done);
+                    } else if (to_global &&
+                               (done <= CHG_RAMP || (done & (args.chg - 1)) < GCOLS)) {
+                        // every group while the next stripe starts up, then
+                        // every chg columns
+                        if (lane == 31) st_release_gpu(args.gprog + b, gbase_out + done);
+                    }
                 }
             }
             // drain: per-step flow control, lanes predicated on their columns
             for (; st < nsteps; ++st) {
                 preamble(st);
-                body(st, true);
+                body(st, true, false);
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
                     const int j = C * (st - 31) + c;
@@ -739,6 +795,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         for (; st < nsteps; ++st) generic(st);
         cp_async_wait<0>();
         __syncwarp();
+        if (args.dbg && lane == 0) {
+            if (warp == 0) args.dbg[s * 4 + 2] = globaltimer();
+            if (warp == wact - 1) args.dbg[s * 4 + 3] = globaltimer();
+        }
     }
 }
 

@@ -3,6 +3,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdio>
+#include <vector>
 
 #include <cstdint>
 #include <algorithm>
@@ -165,11 +167,31 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
     if (!a.gbuf || !a.gprog || !a.gmbuf) return cudaErrorMemoryAllocation;
     e = cudaMemsetAsync(a.gprog, 0, sizeof(long long) * (size_t)G, st);
     if (e != cudaSuccess) return e;
+    // TWB_DBG_TIMES=<file>: per-stripe timestamps (diagnostics, synchronises)
+    const char* dbg_path = getenv("TWB_DBG_TIMES");
+    a.dbg = dbg_path ? (long long*)alloc.get(sizeof(long long) * (4 + 2 * W) * (size_t)S) : nullptr;
     void* params[] = {(void*)&a};
     // Cooperative launch: every CTA must be co-resident (CTA b spins on CTA b-1).
     ctx->before(st);
     e = cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)G), dim3(W * 32), params, smem, st);
     ctx->after(st);
+    if (e == cudaSuccess && a.dbg) {
+        std::vector<long long> h((size_t)S * (4 + 2 * W));
+        cudaMemcpyAsync(h.data(), a.dbg, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st);
+        cudaStreamSynchronize(st);
+        if (FILE* f = fopen(dbg_path, "w")) {
+            fprintf(f, "# S=%lld G=%lld H=%lld nB=%lld chg=%d\n", (long long)S, (long long)G,
+                    (long long)H, (long long)pr.nB, chg);
+            for (int64_t k = 0; k < S; ++k) {
+                fprintf(f, "%lld %lld %lld %lld %lld", (long long)k, h[k * 4], h[k * 4 + 1],
+                        h[k * 4 + 2], h[k * 4 + 3]);
+                for (int w = 0; w < W; ++w) fprintf(f, " %lld", h[S * (4 + W) + k * W + w]);
+                for (int w = 0; w < W; ++w) fprintf(f, " %lld", h[S * 4 + k * W + w]);
+                fprintf(f, "\n");
+            }
+            fclose(f);
+        }
+    }
     return e;
 }
 

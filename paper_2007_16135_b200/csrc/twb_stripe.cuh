@@ -457,7 +457,7 @@ struct LaneRows {
             const Z del_a = zu + da[q];
             Z z;
             if constexpr (sizeof(Z) == 4) z = fminf(pre[q], del_a);
-            else z = chain_min(pre[q], del_a);
+            else z = chain_min<D >= 2 && !F32>(pre[q], del_a);
             zl[q] = z;
             zu = z;
         }
