@@ -25,6 +25,7 @@ _i64 = ctypes.c_int64
 _pd = ctypes.POINTER(ctypes.c_double)
 _pf = ctypes.POINTER(ctypes.c_float)
 _pi64 = ctypes.POINTER(ctypes.c_int64)
+_pi32 = ctypes.POINTER(ctypes.c_int32)
 _vp = ctypes.c_void_p
 
 _SIGS = {
@@ -38,6 +39,10 @@ _SIGS = {
     "twb_selftest_sqrt": (_i64, [_i64, ctypes.c_uint64, _i32, ctypes.POINTER(_i64)]),
     "twb_twed_f64": (ctypes.c_int, [_pd, _i64, _pd, _pd, _i64, _pd, _i32, _d, _d, _i32, _i32, _pd]),
     "twb_twed_f32": (ctypes.c_int, [_pf, _i64, _pf, _pf, _i64, _pf, _i32, _d, _d, _i32, _i32, _pd]),
+    "twb_twed_multi_f64": (ctypes.c_int, [_pd, _i64, _pd, _pd, _i64, _pd, _i32, _d, _d, _i32, _pi32,
+                                          _i32, _pd]),
+    "twb_twed_multi_f32": (ctypes.c_int, [_pf, _i64, _pf, _pf, _i64, _pf, _i32, _d, _d, _i32, _pi32,
+                                          _i32, _pd]),
     "twb_twed_dev_f64": (ctypes.c_int, [_vp, _i64, _vp, _vp, _i64, _vp, _i32, _d, _d, _i32, _vp, _vp]),
     "twb_twed_dev_f32": (ctypes.c_int, [_vp, _i64, _vp, _vp, _i64, _vp, _i32, _d, _d, _i32, _vp, _vp]),
     "twb_twed_batch_f64": (ctypes.c_int, [_pd, _pi64, _i64, _pd, _pd, _pi64, _i64, _pd, _i32, _d, _d,

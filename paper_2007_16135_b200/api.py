@@ -81,7 +81,11 @@ def twed(A, TA, B, TB, nu=1.0, lamb=None, degree=2, *, lam=None, dtype=None, dev
 
 
 def twed_series(a: TimeSeries, b: TimeSeries, params: TwedParams, device=0) -> float:
-    """engine.twed_parallel equivalent on validated series (E:101-121)."""
+    """engine.twed_parallel equivalent on validated series (E:101-121).
+
+    ``device`` is one CUDA device, or a sequence of devices: the pair's
+    wavefront then runs as one ring of CTAs over one kernel per listed device
+    (twb_twed_multi_*; a device may repeat). Same result, bit for bit."""
     if a.d != b.d:
         raise InvalidInputError(f"series dimensions differ: {a.d} vs {b.d}")
     lib = _lib.load()
@@ -89,7 +93,17 @@ def twed_series(a: TimeSeries, b: TimeSeries, params: TwedParams, device=0) -> f
     va, ta = np.ascontiguousarray(a.values), np.ascontiguousarray(a.timestamps)
     vb, tb = np.ascontiguousarray(b.values), np.ascontiguousarray(b.timestamps)
     out = ctypes.c_double(0.0)
-    fn = lib.twb_twed_f64 if va.dtype == np.float64 else lib.twb_twed_f32
+    f64 = va.dtype == np.float64
+    if isinstance(device, (list, tuple, np.ndarray)):
+        devs = np.ascontiguousarray(device, dtype=np.int32)
+        if devs.ndim != 1 or devs.size < 1:
+            raise ValueError("device list must be a non-empty 1-D sequence")
+        fn = lib.twb_twed_multi_f64 if f64 else lib.twb_twed_multi_f32
+        _lib.check(fn(_ptr(va), a.n, _ptr(ta), _ptr(vb), b.n, _ptr(tb), a.d, params.nu,
+                      params.lam, params.degree, devs.ctypes.data_as(_lib._pi32), int(devs.size),
+                      ctypes.byref(out)))
+        return float(out.value)
+    fn = lib.twb_twed_f64 if f64 else lib.twb_twed_f32
     _lib.check(fn(_ptr(va), a.n, _ptr(ta), _ptr(vb), b.n, _ptr(tb), a.d, params.nu, params.lam,
                   params.degree, int(device), ctypes.byref(out)))
     return float(out.value)

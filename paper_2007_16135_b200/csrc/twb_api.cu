@@ -12,6 +12,7 @@
 #include <string>
 #include <type_traits>
 #include <vector>
+#include <functional>
 
 #include "../../include/twb.h"
 #include "twb_dispatch.h"
@@ -327,6 +328,159 @@ int twed_pair_host(const T* A, int64_t nA, const T* TA, const T* B, int64_t nB, 
     if (rc) return rc;
     CK(cudaMemcpyAsync(out, dout, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// One pair on several devices: the wavefront's ring of
+// CTAs spans one kernel per device; every part holds the prepared series, the
+// stripes go round-robin over the whole ring, and the last CTA of each part
+// writes its bottom row straight into the next part's inbox (peer memory over
+// NVLink, system-scope release/acquire on the progress counter). A device may
+// appear more than once (several kernels on one GPU, each on its own stream):
+// the same protocol on one GPU, which is how it is tested here.
+// ---------------------------------------------------------------------------
+template <typename T>
+int twed_pair_multi(const T* A, int64_t nA, const T* TA, const T* B, int64_t nB, const T* TB,
+                    int dim, double nu, double lam, int degree, const int32_t* devices,
+                    int32_t ndev, double* out) {
+    using R = T;
+    using Z = double;
+    int rc = check_params(nA, nB, dim, nu, lam, degree);
+    if (rc) return rc;
+    if (!A || !TA || !B || !TB || !out || !devices) return fail(TWB_EINVAL, "null pointer argument");
+    if (ndev < 1 || ndev > 64) return fail(TWB_EINVAL, "ndev must be in [1, 64], got %d", ndev);
+    int count = 0;
+    CK(cudaGetDeviceCount(&count));
+    for (int q = 0; q < ndev; ++q)
+        if (devices[q] < 0 || devices[q] >= count)
+            return fail(TWB_EINVAL, "device %d out of range (%d devices)", devices[q], count);
+    // the producer part q writes into part q+1's memory
+    for (int q = 0; q < ndev; ++q) {
+        const int a = devices[q], b = devices[(q + 1) % ndev];
+        if (a == b) continue;
+        int ok = 0;
+        CK(cudaDeviceCanAccessPeer(&ok, a, b));
+        if (!ok) return fail(TWB_EUNSUP, "device %d cannot access device %d (no peer access)", a, b);
+        CK(cudaSetDevice(a));
+        cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (e != cudaSuccess) return fail(TWB_ECUDA, "enable peer access %d -> %d: %s", a, b, cudaGetErrorString(e));
+    }
+    struct Part {
+        int dev;
+        cudaStream_t st = nullptr;
+        Scratch* sc = nullptr;
+        R* V[2];
+        R* Tm[2];
+        Z* Del[2];
+        Z* zout;
+        int* dflag;
+    };
+    std::vector<Part> parts(ndev);
+    int* abort_flag = nullptr;
+    auto cleanup = [&]() {
+        for (Part& q : parts) {
+            if (!q.st) continue;
+            cudaSetDevice(q.dev);
+            cudaStreamSynchronize(q.st);
+            delete q.sc;
+            cudaStreamSynchronize(q.st);
+            cudaStreamDestroy(q.st);
+        }
+        if (abort_flag) cudaFreeHost(abort_flag);
+    };
+    struct Guard {
+        std::function<void()> f;
+        ~Guard() { f(); }
+    } guard{cleanup};
+    const double lim = safe_limit<R>();
+    for (int q = 0; q < ndev; ++q) {
+        Part& pt = parts[q];
+        pt.dev = devices[q];
+        CK(cudaSetDevice(pt.dev));
+        init_pool(pt.dev);
+        CK(cudaStreamCreateWithFlags(&pt.st, cudaStreamNonBlocking));
+        pt.sc = new Scratch(pt.st);
+        Scratch& sc = *pt.sc;
+        T* dA = sc.get_n<T>(nA * dim);
+        T* dTA = sc.get_n<T>(nA);
+        T* dB = sc.get_n<T>(nB * dim);
+        T* dTB = sc.get_n<T>(nB);
+        pt.dflag = sc.get_n<int>(1);
+        pt.V[0] = sc.get_n<R>((nA + 1) * dim);
+        pt.V[1] = sc.get_n<R>((nB + 1) * dim);
+        pt.Tm[0] = sc.get_n<R>(nA + 1);
+        pt.Tm[1] = sc.get_n<R>(nB + 1);
+        pt.Del[0] = sc.get_n<Z>(nA + 1);
+        pt.Del[1] = sc.get_n<Z>(nB + 1);
+        pt.zout = sc.get_n<Z>(1);
+        if (sc.failed) return fail(TWB_ENOMEM, "device allocation failed on device %d", pt.dev);
+        CK(cudaMemcpyAsync(dA, A, sizeof(T) * nA * dim, cudaMemcpyHostToDevice, pt.st));
+        CK(cudaMemcpyAsync(dTA, TA, sizeof(T) * nA, cudaMemcpyHostToDevice, pt.st));
+        CK(cudaMemcpyAsync(dB, B, sizeof(T) * nB * dim, cudaMemcpyHostToDevice, pt.st));
+        CK(cudaMemcpyAsync(dTB, TB, sizeof(T) * nB, cudaMemcpyHostToDevice, pt.st));
+        CK(cudaMemsetAsync(pt.dflag, 0, sizeof(int), pt.st));
+        check_unsafe(dA, nA * dim, lim, pt.dflag, pt.st, safe_tiny<R>());
+        check_unsafe(dTA, nA, lim, pt.dflag, pt.st);
+        check_unsafe(dB, nB * dim, lim, pt.dflag, pt.st, safe_tiny<R>());
+        check_unsafe(dTB, nB, lim, pt.dflag, pt.st);
+        if ((rc = prepare<T, R, Z>(dA, dTA, nullptr, 1, nA, nA, dim, nu, lam, degree, pt.V[0],
+                                   pt.Tm[0], pt.Del[0], pt.st)))
+            return rc;
+        if ((rc = prepare<T, R, Z>(dB, dTB, nullptr, 1, nB, nB, dim, nu, lam, degree, pt.V[1],
+                                   pt.Tm[1], pt.Del[1], pt.st)))
+            return rc;
+    }
+    int hflag = 0;
+    CK(cudaSetDevice(parts[0].dev));
+    CK(cudaMemcpyAsync(&hflag, parts[0].dflag, sizeof(int), cudaMemcpyDeviceToHost, parts[0].st));
+    CK(cudaStreamSynchronize(parts[0].st));
+    Variant v = pick_variant(dim, degree, nu, lam, hflag != 0, lim);
+    int ra = 0, rb = 1;
+    int64_t na = nA, nb = nB;
+    if (!v.E && nB > nA) {  // rows = the longer series (exact symmetry, safe mode)
+        ra = 1;
+        rb = 0;
+        std::swap(na, nb);
+    }
+    CK(cudaHostAlloc((void**)&abort_flag, sizeof(int), cudaHostAllocMapped | cudaHostAllocPortable));
+    *abort_flag = 0;
+    std::vector<WavePart<R, Z>> wp(ndev);
+    for (int q = 0; q < ndev; ++q) {
+        Part& pt = parts[q];
+        CK(cudaStreamSynchronize(pt.st));  // inputs prepared on every part
+        wp[q] = WavePart<R, Z>{pt.dev, pt.st, {pt.V[ra], pt.Tm[ra], pt.Del[ra]},
+                               {pt.V[rb], pt.Tm[rb], pt.Del[rb]}, pt.zout,
+                               Alloc{scratch_alloc, pt.sc}};
+    }
+    long long timeout_ms = 20000;
+    if (const char* env = getenv("TWB_RING_TIMEOUT_MS")) timeout_ms = atoll(env);
+    CtaRing<R, Z> ring{ndev, wp.data(), abort_flag, timeout_ms * 1000000LL};
+    WaveProblem<R, Z> pr;
+    pr.A = wp[0].A;
+    pr.B = wp[0].B;
+    pr.nA = na;
+    pr.nB = nb;
+    pr.nu = nu;
+    pr.p = degree;
+    pr.out = wp[0].out;
+    pr.ring = &ring;
+    CK(cudaSetDevice(parts[0].dev));
+    CK(call_wave<R, Z>(dim, v.P, v.E, v.N1, pr, *parts[0].sc, parts[0].st));
+    for (Part& pt : parts) {
+        CK(cudaSetDevice(pt.dev));
+        CK(cudaStreamSynchronize(pt.st));
+        if (pt.sc->failed) return fail(TWB_ENOMEM, "device scratch allocation failed on device %d", pt.dev);
+    }
+    if (*(volatile int*)abort_flag)
+        return fail(TWB_ECUDA, "multi-device sweep aborted: a stripe waited %lld ms for its producer "
+                    "(kernels of the ring not co-resident?)", timeout_ms);
+    if (ring.owner < 0) return fail(TWB_ECUDA, "multi-device sweep: no owner of the last stripe");
+    const Part& own = parts[ring.owner];
+    CK(cudaSetDevice(own.dev));
+    CK(cudaMemcpyAsync(out, own.zout, sizeof(double), cudaMemcpyDeviceToHost, own.st));
+    CK(cudaStreamSynchronize(own.st));
     return 0;
 }
 
@@ -792,6 +946,18 @@ int twb_twed_dev_f32(const float* dA, int64_t nA, const float* dTA, const float*
     if (rc) return rc;
     return twed_pair_dev<float, float, double>(dA, nA, dTA, dB, nB, dTB, dim, nu, lam, degree,
                                                (cudaStream_t)stream, d_out);
+}
+
+int twb_twed_multi_f64(const double* A, int64_t nA, const double* TA, const double* B, int64_t nB,
+                       const double* TB, int32_t dim, double nu, double lam, int32_t degree,
+                       const int32_t* devices, int32_t ndev, double* out) {
+    return twed_pair_multi<double>(A, nA, TA, B, nB, TB, dim, nu, lam, degree, devices, ndev, out);
+}
+
+int twb_twed_multi_f32(const float* A, int64_t nA, const float* TA, const float* B, int64_t nB,
+                       const float* TB, int32_t dim, double nu, double lam, int32_t degree,
+                       const int32_t* devices, int32_t ndev, double* out) {
+    return twed_pair_multi<float>(A, nA, TA, B, nB, TB, dim, nu, lam, degree, devices, ndev, out);
 }
 
 int twb_twed_batch_f64(const double* AA, const int64_t* a_off, int64_t nAA, const double* TAA,

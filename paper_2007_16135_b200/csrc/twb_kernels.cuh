@@ -397,9 +397,24 @@ struct WaveArgs {
     int64_t nA, nB;
     int64_t S;  // stripes
     int64_t H;  // rows per stripe
-    Z* gbuf;            // gridDim.x x (nB+1): bottom row z of the CTA's current stripe
-    R* gmbuf;           // gridDim.x x (nB+1): bottom row d(r, j) / c(r, j)
-    long long* gprog;   // gridDim.x progress counters: stripe*(nB+1) + columns published
+    // Inboxes: slot b holds the bottom row (z, d / c) of the stripe above the
+    // one CTA b is sweeping, written by the CTA before it in the ring, and
+    // that producer's progress counter (stripe*(nB+1) + columns published).
+    Z* gbuf;            // gridDim.x x (nB+1)
+    R* gmbuf;           // gridDim.x x (nB+1)
+    long long* gprog;   // gridDim.x
+    // The ring of CTAs may span several kernels (one per device, or several
+    // on one device): this kernel's CTAs are ring positions cta0 .. cta0+G-1
+    // of GT; stripe s belongs to ring position s % GT. The last CTA feeds the
+    // next kernel's CTA 0 through next_* (a peer pointer across devices; for a
+    // single kernel next_* = slot 0 of the own inboxes).
+    int64_t cta0, GT;
+    Z* next_z;
+    R* next_m;
+    long long* next_prog;
+    int sys;            // publish / poll the cross-kernel links at system scope
+    int* abort;         // multi-kernel rings: set on a wait timeout (null: no timeout)
+    long long timeout_ns;
     int chg;            // publish granularity of the bottom row (power of 2, >= 32)
     double nu;
     int p;
@@ -442,7 +457,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
     const int lane = threadIdx.x & 31;
     const int G = gridDim.x;
     const int b = blockIdx.x;
-    const int pb = (b + G - 1) % G;
+    const int64_t gb = args.cta0 + b;  // ring position
+    __shared__ int s_abort;
+    if (threadIdx.x == 0) s_abort = 0;
+    auto s_abort_seen = [&]() { return args.abort != nullptr && *(volatile int*)&s_abort != 0; };
+    // cross-kernel links: CTA 0 polls a producer in another kernel, the last
+    // CTA publishes to one
+    const bool sys_in = args.sys && b == 0;
+    const bool sys_out = args.sys && b == G - 1;
     Ring& ring = rings[warp];
     const Z INF = zinf<Z>();
     const int ncols = (int)(args.nB + 1);
@@ -457,7 +479,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
     const int own_lane = (int)((loc_last / K) % 32);
     const int own_q = (int)(loc_last % K);
 
-    for (int64_t s = b; s < args.S; s += G) {
+    for (int64_t s = gb; s < args.S; s += args.GT) {
         __syncthreads();
         if (threadIdx.x < WARPS) {
             prog[threadIdx.x] = 0;
@@ -485,10 +507,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         const bool owner = s == s_last && warp == own_warp && lane == own_lane;
         const long long gbase_in = (long long)(s - 1) * ncols;
         const long long gbase_out = (long long)s * ncols;
-        Z* grow_out = args.gbuf + (int64_t)b * ncols;
-        const Z* grow_in = args.gbuf + (int64_t)pb * ncols;
-        R* gmrow_out = args.gmbuf + (int64_t)b * ncols;
-        const R* gmrow_in = args.gmbuf + (int64_t)pb * ncols;
+        // own inbox in, the next ring position's inbox out
+        const Z* grow_in = args.gbuf + (int64_t)b * ncols;
+        const R* gmrow_in = args.gmbuf + (int64_t)b * ncols;
+        Z* grow_out = b + 1 < G ? args.gbuf + (int64_t)(b + 1) * ncols : args.next_z;
+        R* gmrow_out = b + 1 < G ? args.gmbuf + (int64_t)(b + 1) * ncols : args.next_m;
+        long long* prog_out = b + 1 < G ? args.gprog + b + 1 : args.next_prog;
 
         // Previous stripe's bottom row (warp 0 of a non-top stripe): the 32C
         // columns of the next 32 steps are loaded into registers one block
@@ -498,7 +522,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         R pm[C];
         auto fetch = [&](int c0) {  // columns [c0, c0 + 32C) -> registers
             const long long need = gbase_in + min(c0 + 32 * C, ncols);
-            if (TWB_DBG_NOSYNC < 1) gwait(args.gprog + pb, need);
+            if (TWB_DBG_NOSYNC < 1) {
+                if (args.abort) {  // multi-kernel ring: bounded wait
+                    if (!gwait_bounded(args.gprog + b, need, sys_in, args.abort, args.timeout_ns))
+                        s_abort = 1;
+                } else {
+                    gwait(args.gprog + b, need);
+                }
+            }
 #pragma unroll
             for (int k = 0; k < C; ++k) {
                 const int c = c0 + 32 * k + lane;
@@ -534,12 +565,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             if (warp > 0 && (st % CHS) == 0 && C * st < ncols) {
                 if (lane == 0) st_release_cta(&cons[warp], C * st);
                 const int need = min(C * (st + CHS), ncols);
-                while (TWB_DBG_NOSYNC < 2 && ld_acquire_cta(&prog[warp]) < need) spin_pause();
+                while (TWB_DBG_NOSYNC < 2 && ld_acquire_cta(&prog[warp]) < need && !s_abort_seen())
+                    spin_pause();
             }
             const int j31 = C * (st - 31);  // lane 31's first column this step
             if (to_ring && j31 >= 0 && j31 < ncols && (j31 % GCOLS) == 0) {
                 const int need = j31 + GCOLS - ZRS;
-                while (TWB_DBG_NOSYNC < 2 && ld_acquire_cta(&cons[warp + 1]) < need) spin_pause();
+                while (TWB_DBG_NOSYNC < 2 && ld_acquire_cta(&cons[warp + 1]) < need &&
+                       !s_abort_seen())
+                    spin_pause();
             }
         };
         // The row above lane 0 at column C*st + c, read by every lane from a
@@ -581,7 +615,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                     if (lane == 31) st_release_cta(&prog[warp + 1], j + 1);
             } else if (to_global) {
                 if (((j + 1) & (args.chg - 1)) == 0 || j == ncols - 1)
-                    if (lane == 31) st_release_gpu(args.gprog + b, gbase_out + j + 1);
+                    if (lane == 31) publish_gpu(prog_out, gbase_out + j + 1, sys_out);
             }
         };
         // Lane 31's bottom row at column j -> next warp / next stripe.
@@ -760,7 +794,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                 preamble(st);
                 if (to_ring) {  // lane 31 writes columns < C*(st0 - 15) this group
                     const int need = C * (st0 - 15) - ZRS;
-                    while (TWB_DBG_NOSYNC < 2 && ld_acquire_cta(&cons[warp + 1]) < need) spin_pause();
+                    while (TWB_DBG_NOSYNC < 2 && ld_acquire_cta(&cons[warp + 1]) < need &&
+                           !s_abort_seen())
+                        spin_pause();
                 }
                 if (st0 < 32) {
                     for (int i = 0; i < CHS; ++i) body(st0 + i, false, true);
@@ -777,7 +813,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                                (done <= CHG_RAMP || (done & (args.chg - 1)) < GCOLS)) {
                         // every group while the next stripe starts up, then
                         // every chg columns
-                        if (lane == 31) st_release_gpu(args.gprog + b, gbase_out + done);
+                        if (lane == 31) publish_gpu(prog_out, gbase_out + done, sys_out);
                     }
                 }
             }

@@ -43,6 +43,26 @@ struct Alloc {
     void* get(size_t bytes) const { return fn(ctx, bytes); }
 };
 
+// One kernel of a CTA ring that spans several kernels (one per device, or
+// several on one device): its device, stream, the prepared series on that
+// device, its result slot and scratch allocator.
+template <typename R, typename Z>
+struct WavePart {
+    int device;
+    cudaStream_t st;
+    PreparedT<R, Z> A, B;
+    Z* out;
+    Alloc alloc;
+};
+template <typename R, typename Z>
+struct CtaRing {
+    int nparts;
+    WavePart<R, Z>* parts;
+    int* abort;             // host-mapped flag, raised by a timed-out wait
+    long long timeout_ns;
+    int owner = -1;         // out: the part whose out slot holds the distance
+};
+
 template <typename R, typename Z>
 struct WaveProblem {
     PreparedT<R, Z> A, B;
@@ -50,6 +70,7 @@ struct WaveProblem {
     double nu;
     int p;
     Z* out;  // device, one value
+    CtaRing<R, Z>* ring = nullptr;  // multi-kernel ring (A, B, out, alloc, st per part)
 };
 
 // Batch kernel variants (lanes per series LW, rows per lane K): row-side
@@ -94,16 +115,37 @@ template <int D, int K, int C, int P, bool E, bool N1, int W, int MINB, typename
 cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream_t st,
                          LaunchCtx* ctx) {
     auto kern = wave_kernel<D, K, C, P, E, N1, W, MINB, R, Z>;
-    int sms = 0, dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t smem = wave_smem<D, R, Z, C, K>(W);
-    int occ = 0;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * 32, smem);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) return cudaErrorLaunchOutOfResources;
+    // The parts of the ring: one (this device, this stream) unless pr.ring.
+    std::vector<WavePart<R, Z>> parts;
+    if (pr.ring) {
+        parts.assign(pr.ring->parts, pr.ring->parts + pr.ring->nparts);
+    } else {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        parts.push_back(WavePart<R, Z>{dev, st, pr.A, pr.B, pr.out, alloc});
+    }
+    const int np = (int)parts.size();
+    int cur_dev = 0;
+    cudaGetDevice(&cur_dev);
+    // SM slots per part (parts sharing a device split it)
+    std::vector<int64_t> capp(np);
+    int64_t cap = 0;
+    for (int q = 0; q < np; ++q) {
+        int sms = 0, occ = 0, share = 0;
+        for (int r = 0; r < np; ++r) share += parts[r].device == parts[q].device;
+        cudaError_t e = cudaSetDevice(parts[q].device);
+        if (e == cudaSuccess)
+            e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, parts[q].device);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * 32, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < 1) return cudaErrorLaunchOutOfResources;
+        capp[q] = (int64_t)sms * occ / share;
+        cap += capp[q];
+    }
+    cudaSetDevice(cur_dev);
     // Stripe height: ws active warps of 32*K rows (ws <= W). Every stripe
     // sweeps all nB+1 columns, so a round of G co-resident stripes costs about
     // nB steps however many rows it holds, and the pipeline fill adds
@@ -111,7 +153,6 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
     // stripes fill every SM slot in the fewest rounds (e.g. n = 1M, K = 8:
     // 7 warps -> 559 stripes = 3.8 rounds of 148, instead of 8 warps -> 489
     // stripes on only 123 SMs).
-    const int64_t cap = (int64_t)sms * occ;
     int64_t H = 0, S = 0, G = 0;
     double best = 0;
     // TWB_WAVE_WS=<n> pins the active warps per stripe (tuning experiments).
@@ -143,13 +184,19 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
             G = g;
         }
     }
-    WaveArgs<R, Z> a;
-    a.A = pr.A;
-    a.B = pr.B;
-    a.nA = pr.nA;
-    a.nB = pr.nB;
-    a.S = S;
-    a.H = H;
+    // Ring positions per part, in proportion to their SM slots; parts left
+    // without a CTA drop out of the ring.
+    std::vector<int64_t> gp(np, 0);
+    {
+        int64_t given = 0;
+        for (int q = 0; q < np; ++q) given += gp[q] = std::min(capp[q], G * capp[q] / cap);
+        for (int q = 0; given < G; q = (q + 1) % np)
+            if (gp[q] < capp[q]) ++gp[q], ++given;
+    }
+    std::vector<int> live;
+    for (int q = 0; q < np; ++q)
+        if (gp[q] > 0) live.push_back(q);
+    const int nl = (int)live.size();
     // Bottom-row publish granularity: every st.release.gpu costs the
     // producing warp a GPU-scope fence, so publish every chg columns (more for
     // long rows; the consumer lags far behind anyway). TWB_WAVE_CHG overrides.
@@ -157,27 +204,65 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
     while (chg < 256 && (int64_t)chg * 2048 <= pr.nB) chg *= 2;
     if (const char* env = getenv("TWB_WAVE_CHG")) chg = atoi(env);
     if (chg < 32 || (chg & (chg - 1))) chg = 32;
-    a.chg = chg;
-    a.nu = pr.nu;
-    a.p = pr.p;
-    a.out = pr.out;
-    a.gbuf = (Z*)alloc.get(sizeof(Z) * (size_t)G * (size_t)(pr.nB + 1));
-    a.gmbuf = (R*)alloc.get(sizeof(R) * (size_t)G * (size_t)(pr.nB + 1));
-    a.gprog = (long long*)alloc.get(sizeof(long long) * (size_t)G);
-    if (!a.gbuf || !a.gprog || !a.gmbuf) return cudaErrorMemoryAllocation;
-    e = cudaMemsetAsync(a.gprog, 0, sizeof(long long) * (size_t)G, st);
-    if (e != cudaSuccess) return e;
-    // TWB_DBG_TIMES=<file>: per-stripe timestamps (diagnostics, synchronises)
-    const char* dbg_path = getenv("TWB_DBG_TIMES");
-    a.dbg = dbg_path ? (long long*)alloc.get(sizeof(long long) * (4 + 2 * W) * (size_t)S) : nullptr;
-    void* params[] = {(void*)&a};
-    // Cooperative launch: every CTA must be co-resident (CTA b spins on CTA b-1).
-    ctx->before(st);
-    e = cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)G), dim3(W * 32), params, smem, st);
-    ctx->after(st);
-    if (e == cudaSuccess && a.dbg) {
+    const size_t ncols = (size_t)(pr.nB + 1);
+    std::vector<WaveArgs<R, Z>> args(nl);
+    int64_t cta0 = 0;
+    const int64_t pos_last = ((pr.nA - 1) / H) % G;  // ring position of the last stripe
+    for (int l = 0; l < nl; ++l) {
+        const WavePart<R, Z>& pt = parts[live[l]];
+        WaveArgs<R, Z>& a = args[l];
+        cudaSetDevice(pt.device);
+        a.A = pt.A;
+        a.B = pt.B;
+        a.nA = pr.nA;
+        a.nB = pr.nB;
+        a.S = S;
+        a.H = H;
+        a.chg = chg;
+        a.nu = pr.nu;
+        a.p = pr.p;
+        a.out = pt.out;
+        const int64_t g = gp[live[l]];
+        a.gbuf = (Z*)pt.alloc.get(sizeof(Z) * (size_t)g * ncols);
+        a.gmbuf = (R*)pt.alloc.get(sizeof(R) * (size_t)g * ncols);
+        a.gprog = (long long*)pt.alloc.get(sizeof(long long) * (size_t)g);
+        if (!a.gbuf || !a.gprog || !a.gmbuf) return cudaErrorMemoryAllocation;
+        cudaError_t e = cudaMemsetAsync(a.gprog, 0, sizeof(long long) * (size_t)g, pt.st);
+        if (e != cudaSuccess) return e;
+        a.cta0 = cta0;
+        a.GT = G;
+        if (pos_last >= cta0 && pos_last < cta0 + g && pr.ring) pr.ring->owner = live[l];
+        cta0 += g;
+        a.sys = nl > 1;
+        a.abort = nl > 1 ? pr.ring->abort : nullptr;
+        a.timeout_ns = pr.ring ? pr.ring->timeout_ns : 0;
+        a.dbg = nullptr;
+    }
+    for (int l = 0; l < nl; ++l) {  // the last CTA of each part feeds the next part's CTA 0
+        const WaveArgs<R, Z>& nx = args[(l + 1) % nl];
+        args[l].next_z = nx.gbuf;
+        args[l].next_m = nx.gmbuf;
+        args[l].next_prog = nx.gprog;
+    }
+    // TWB_DBG_TIMES=<file>: per-stripe timestamps (single kernel; diagnostics, synchronises)
+    const char* dbg_path = nl == 1 && !pr.ring ? getenv("TWB_DBG_TIMES") : nullptr;
+    if (dbg_path) args[0].dbg = (long long*)alloc.get(sizeof(long long) * (4 + 2 * W) * (size_t)S);
+    // Cooperative launch: every CTA of a kernel is co-resident (CTA b spins on
+    // CTA b-1); the kernels of a ring are launched in ring order.
+    cudaError_t e = cudaSuccess;
+    for (int l = 0; l < nl && e == cudaSuccess; ++l) {
+        const WavePart<R, Z>& pt = parts[live[l]];
+        cudaSetDevice(pt.device);
+        void* params[] = {(void*)&args[l]};
+        if (l == 0) ctx->before(pt.st);
+        e = cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)gp[live[l]]),
+                                        dim3(W * 32), params, smem, pt.st);
+        if (l == 0) ctx->after(pt.st);
+    }
+    cudaSetDevice(cur_dev);
+    if (e == cudaSuccess && dbg_path) {
         std::vector<long long> h((size_t)S * (4 + 2 * W));
-        cudaMemcpyAsync(h.data(), a.dbg, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(h.data(), args[0].dbg, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, st);
         cudaStreamSynchronize(st);
         if (FILE* f = fopen(dbg_path, "w")) {
             fprintf(f, "# S=%lld G=%lld H=%lld nB=%lld chg=%d\n", (long long)S, (long long)G,
@@ -201,6 +286,16 @@ cudaError_t run_wave(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream
     int sms = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (pr.ring && pr.ring->nparts > 1) {  // SMs of the whole ring
+        sms = 0;
+        for (int q = 0; q < pr.ring->nparts; ++q) {
+            int share = 0, m = 0;
+            for (int r = 0; r < pr.ring->nparts; ++r)
+                share += pr.ring->parts[r].device == pr.ring->parts[q].device;
+            cudaDeviceGetAttribute(&m, cudaDevAttrMultiProcessorCount, pr.ring->parts[q].device);
+            sms += m / share;
+        }
+    }
     // TWB_WAVE_CFG pins a variant (tuning experiments; proven-safe modes):
     // k<rows per lane>w<warps per CTA>[c<columns per step>]
     if constexpr (!E) {

@@ -1,0 +1,72 @@
+"""One pair over several devices (twb_twed_multi_*).
+
+The run has one B200, so the ring of CTAs is split over several kernels on
+that one device (``device=[0, 0]``): each kernel is its own cooperative launch
+on its own stream, the last CTA of each part feeds the next part's CTA 0
+through its inbox with system-scope release/acquire, exactly the protocol of
+the multi-GPU case minus the NVLink hop. Results must be bit-identical to the
+single-kernel sweep and to the reference goldens.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+from conftest import has_cuda
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")]
+
+os.environ.setdefault("TWB_RING_TIMEOUT_MS", "15000")
+
+
+@pytest.fixture(scope="module")
+def twb():
+    import paper_2007_16135_b200 as twb
+    return twb
+
+
+@pytest.mark.parametrize("parts", [[0, 0], [0, 0, 0], [0, 0, 0, 0]])
+def test_ring_parts_match_single_kernel(twb, config_golden, parts):
+    from paper_2007_16135_b200.workloads import make_pair
+    g = config_golden["cfg2"]  # n = 100k, d = 1 (the reference's own value)
+    a, ta, b, tb = make_pair(100_000, 1, 1)
+    assert twb.twed(a, ta, b, tb, 1.0, 1.0, 2, device=parts) == g["value"]
+    for key in ("walk_8192_d3_s13", "walk_20000_d1_s14"):
+        g = config_golden[key]
+        a, ta, b, tb = make_pair(g["n"], g["d"], g["seed"])
+        assert twb.twed(a, ta, b, tb, 1.0, 1.0, 2, device=parts) == g["value"], key
+
+
+def test_ring_long_pair_d3(twb):
+    """Several rounds of stripes over the ring (n = 400k, d = 3)."""
+    from paper_2007_16135_b200.workloads import make_pair
+    a, ta, b, tb = make_pair(400_000, 3, 21)
+    one = twb.twed(a, ta, b, tb, 1.0, 1.0, 2)
+    assert twb.twed(a, ta, b, tb, 1.0, 1.0, 2, device=[0, 0]) == one
+    assert twb.twed(a, ta, b, tb, 1.0, 1.0, 2, device=[0, 0, 0]) == one
+
+
+def test_ring_ragged_irregular_fp32_and_nan(twb):
+    rng = np.random.default_rng(5)
+    a = np.cumsum(rng.standard_normal((37_001, 2)), axis=0)
+    b = np.cumsum(rng.standard_normal((52_333, 2)), axis=0)
+    ta = np.cumsum(rng.uniform(0.05, 2.0, len(a)))
+    tb = np.cumsum(rng.uniform(0.05, 2.0, len(b)))
+    for nu, lam in ((1.0, 1.0), (0.25, 0.5)):
+        one = twb.twed(a, ta, b, tb, nu, lam, 2)
+        assert twb.twed(a, ta, b, tb, nu, lam, 2, device=[0, 0]) == one
+    one = twb.twed(a, ta, b, tb, 1.0, 1.0, 2, dtype=np.float32)
+    assert twb.twed(a, ta, b, tb, 1.0, 1.0, 2, dtype=np.float32, device=[0, 0]) == one
+    a2 = a.copy()
+    a2[20_000, 1] = np.nan  # NaN-exact mode (compare chain, no swap)
+    one = twb.twed(a2, ta, b, tb, 1.0, 1.0, 2)
+    got = twb.twed(a2, ta, b, tb, 1.0, 1.0, 2, device=[0, 0])
+    assert (np.isnan(one) and np.isnan(got)) or got == one
+
+
+def test_ring_bad_device_raises(twb):
+    a = np.arange(100.0)
+    with pytest.raises(ValueError, match="out of range"):
+        twb.twed(a, a, a, a, 1.0, 1.0, 2, device=[0, 99])
