@@ -377,6 +377,8 @@ def run_ours(args, world, rank, local):
     if not args.no_batch:
         batch = run_batch_cfg5(args, world, rank, local)
     extra = {} if args.no_extra else run_extra(args, world, rank, local)
+    if world > 1 and not args.no_extra:
+        extra["cfg3_one_pair_all_gpus"] = run_pair_all_gpus(args, world, rank, host)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -463,6 +465,37 @@ def run_extra(args, world, rank, local):
     res["cfg4"] = {"pairs": 1_000_000, "kernel_ms": kms, "pairs_per_s": 1e6 / (kms * 1e-3),
                    "gcups": 1e6 * 256 * 256 / (kms * 1e-3) / 1e9, "n_gpus": world,
                    "sharding": "rows, no collective in the timed kernel"}
+    return res
+
+
+def run_pair_all_gpus(args, world, rank, host):
+    """The headline pair as ONE distance over all N GPUs:
+    rank 0 drives one kernel per device (twb_twed_multi_*, peer memory between
+    consecutive devices) through the public API with host arrays; the other
+    ranks keep their GPUs idle behind a CPU-side (gloo) barrier -- an NCCL
+    barrier kernel would hold SMs the cooperative launches need."""
+    import torch.distributed as dist
+
+    import paper_2007_16135_b200 as twb
+
+    grp = dist.new_group(backend="gloo")
+    dist.barrier(group=grp)
+    res = None
+    if rank == 0:
+        try:
+            a, ta, b, tb = host
+            n = len(a)
+            twb.twed(a[:4096], ta[:4096], b[:4096], tb[:4096], 1.0, 1.0, 2,
+                     device=list(range(world)))  # warm: contexts, peer access
+            t0 = time.perf_counter()
+            r = twb.twed(a, ta, b, tb, 1.0, 1.0, 2, device=list(range(world)))
+            dt = time.perf_counter() - t0
+            res = {"n_gpus": world, "ms": dt * 1e3, "gcups": n * n / dt / 1e9, "result": r,
+                   "timing": "wall clock, host arrays (H2D + prepare + sweep + D2H), one run",
+                   "path": "twb_twed_multi_f64: one CTA ring over one kernel per GPU"}
+        except Exception as exc:  # report, do not fail the bench line
+            res = {"n_gpus": world, "error": repr(exc)}
+    dist.barrier(group=grp)
     return res
 
 
