@@ -66,6 +66,9 @@ def _load():
             ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_int64, ctypes.c_int,
         ]
         lib.orc_twed_batch.restype = ctypes.c_int
+        lib.orc_lcs_band.restype = ctypes.c_int64
+        lib.orc_lcs_band.argtypes = [ctypes.POINTER(ctypes.c_int64), ctypes.c_int64,
+                                     ctypes.POINTER(ctypes.c_int64), ctypes.c_int64]
         lib.orc_twed_batch.argtypes = [
             _c_double_p, _c_double_p, _c_int64_p, ctypes.c_int64,
             _c_double_p, _c_double_p, _c_int64_p, ctypes.c_int64,
@@ -193,3 +196,28 @@ def host_description() -> dict:
     except OSError:
         pass
     return {"cpu_count": os.cpu_count(), "model": model, "omp_threads": max_threads()}
+
+
+def encode_symbols(s, t):
+    """core._encode_symbols (C:141-160): strings -> code points, other
+    sequences -> one shared first-seen code table."""
+    if isinstance(s, str) and isinstance(t, str):
+        return (np.array([ord(c) for c in s], dtype=np.int64),
+                np.array([ord(c) for c in t], dtype=np.int64))
+    codes = {}
+
+    def enc(seq):
+        return np.array([codes.setdefault(x, len(codes)) for x in list(seq)], dtype=np.int64)
+
+    return enc(s), enc(t)
+
+
+def lcs(s, t) -> int:
+    """LCS length, band.lcs_band (band.py:185-197) -> _kernels.lcs_band_solve (K:193-219)."""
+    a, b = encode_symbols(s, t) if not isinstance(s, np.ndarray) else (
+        np.ascontiguousarray(s, dtype=np.int64), np.ascontiguousarray(t, dtype=np.int64))
+    pi = ctypes.POINTER(ctypes.c_int64)
+    r = _load().orc_lcs_band(a.ctypes.data_as(pi), a.size, b.ctypes.data_as(pi), b.size)
+    if r < 0:
+        raise MemoryError("oracle: out of memory")
+    return int(r)

@@ -11,6 +11,7 @@ All compute runs in libtwb200.so; there is no CPU fallback.
 from .api import (
     band_solve,
     batch_matrix,
+    lcs,
     mirror_upper_dev,
     prepare_series,
     twed,
@@ -32,6 +33,7 @@ __all__ = [
     "band_solve",
     "batch_matrix",
     "device_count",
+    "lcs",
     "mirror_upper_dev",
     "prepare_series",
     "twed",

@@ -43,6 +43,7 @@ _SIGS = {
                                           _i32, _pd]),
     "twb_twed_multi_f32": (ctypes.c_int, [_pf, _i64, _pf, _pf, _i64, _pf, _i32, _d, _d, _i32, _pi32,
                                           _i32, _pd]),
+    "twb_lcs_i32": (ctypes.c_int, [_pi32, _i64, _pi32, _i64, _i32, _i32, _pi64]),
     "twb_twed_dev_f64": (ctypes.c_int, [_vp, _i64, _vp, _vp, _i64, _vp, _i32, _d, _d, _i32, _vp, _vp]),
     "twb_twed_dev_f32": (ctypes.c_int, [_vp, _i64, _vp, _vp, _i64, _vp, _i32, _d, _d, _i32, _vp, _vp]),
     "twb_twed_batch_f64": (ctypes.c_int, [_pd, _pi64, _i64, _pd, _pd, _pi64, _i64, _pd, _i32, _d, _d,

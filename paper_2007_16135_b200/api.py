@@ -311,3 +311,62 @@ def mirror_upper_dev(M, stream=None):
     with torch.cuda.device(M.device):
         _lib.check(fn(M.data_ptr(), M.shape[0], st.cuda_stream))
     return M
+
+
+# ---------------------------------------------------------------------------
+# LCS length (band.lcs_band, pkg/src/twedband/band.py:185-197).
+# ---------------------------------------------------------------------------
+def _encode_symbols(s, t):
+    """core._encode_symbols (C:141-160): strings use code points, other
+    sequences of hashable symbols share one first-seen code table."""
+    if isinstance(s, str) and isinstance(t, str):
+        return (np.array([ord(c) for c in s], dtype=np.int64),
+                np.array([ord(c) for c in t], dtype=np.int64))
+    codes: dict = {}
+
+    def encode(seq):
+        out = np.empty(len(seq), dtype=np.int64)
+        for i, sym in enumerate(seq):
+            out[i] = codes.setdefault(sym, len(codes))
+        return out
+
+    return encode(list(s)), encode(list(t))
+
+
+def lcs(s, t, device=0) -> int:
+    """Longest-common-subsequence length of two strings or sequences of
+    hashable symbols; empty inputs give 0 (reference: band.lcs_band). Runs the
+    bit-parallel sweep of libtwb200 (twb_lcs_i32); integer-exact."""
+    a, b = _encode_symbols(s, t)
+    if a.size == 0 or b.size == 0:
+        return 0
+    _lib.require_device()
+    return lcs_codes(a, b, device=device)
+
+
+def dense_codes(a, b):
+    """int64 symbol codes -> int32 codes in [0, A) for the A symbols present in
+    both sequences, -1 for the rest (they can never match)."""
+    a = np.asarray(a, dtype=np.int64)
+    b = np.asarray(b, dtype=np.int64)
+    common = np.intersect1d(a, b)
+    if common.size == 0:
+        return (np.full(a.size, -1, np.int32), np.full(b.size, -1, np.int32), 0)
+    ia = np.minimum(np.searchsorted(common, a), common.size - 1)
+    ib = np.minimum(np.searchsorted(common, b), common.size - 1)
+    ca = np.where(common[ia] == a, ia, -1).astype(np.int32)
+    cb = np.where(common[ib] == b, ib, -1).astype(np.int32)
+    return np.ascontiguousarray(ca), np.ascontiguousarray(cb), int(common.size)
+
+
+def lcs_codes(a, b, device=0) -> int:
+    """LCS length of two int64 code sequences through twb_lcs_i32."""
+    ca, cb, A = dense_codes(a, b)
+    if ca.size == 0 or cb.size == 0:
+        return 0
+    lib = _lib.load()
+    out = ctypes.c_int64(0)
+    pi = ctypes.POINTER(ctypes.c_int32)
+    _lib.check(lib.twb_lcs_i32(ca.ctypes.data_as(pi), ca.size, cb.ctypes.data_as(pi), cb.size,
+                               A, int(device), ctypes.byref(out)))
+    return int(out.value)

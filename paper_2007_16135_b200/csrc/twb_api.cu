@@ -830,6 +830,14 @@ __global__ void sqrt_check_kernel(int64_t n, unsigned long long seed, unsigned l
 
 }  // namespace
 
+// Hooks for the other translation units of the library (twb_lcs.cu): the
+// thread-local error text, launch count and kernel-timing context.
+namespace twb {
+int api_fail(int code, const char* msg) { return fail(code, "%s", msg); }
+void api_count_launch() { ++t_launches; }
+LaunchCtx* api_ctx_begin() { return ctx_begin(); }
+}  // namespace twb
+
 extern "C" {
 
 int64_t twb_selftest_sqrt(int64_t n, uint64_t seed, int32_t device, int64_t* fast_count) {

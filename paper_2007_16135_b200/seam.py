@@ -54,6 +54,13 @@ def band_solve(z, z1, z2, va, ta, del_a, vb, tb, del_b, nu, p, device=0) -> floa
     return float(out.value)
 
 
+def lcs_solve(z, z1, z2, s, t, device=0) -> int:
+    """S2 seam for LCS (_kernels.py:193-219, lcs_band_solve) on libtwb200: the
+    int64 symbol codes of core._encode_symbols in, the LCS length out."""
+    from .api import lcs_codes
+    return lcs_codes(s, t, device=device)
+
+
 class Installed:
     """Handle returned by ``install``; ``restore()`` puts the CPU kernels back."""
 
@@ -68,18 +75,25 @@ class Installed:
 
 
 def install(twedband_module=None, device=0) -> Installed:
-    """Point ``twedband._kernels.twed_band_serial/_parallel`` at the GPU sweep."""
+    """Point ``twedband._kernels.twed_band_serial/_parallel`` (and
+    ``lcs_band_solve``) at the GPU sweeps."""
     if twedband_module is None:
         import twedband as twedband_module  # the reference package
     kernels = twedband_module._kernels
     _lib.require_device()
-    saved = {name: getattr(kernels, name) for name in ("twed_band_serial", "twed_band_parallel")}
+    names = ("twed_band_serial", "twed_band_parallel", "lcs_band_solve")
+    saved = {name: getattr(kernels, name) for name in names}
     handle = Installed(kernels, saved)
 
     def gpu_band(z, z1, z2, va, ta, del_a, vb, tb, del_b, nu, p):
         handle.calls += 1
         return band_solve(z, z1, z2, va, ta, del_a, vb, tb, del_b, nu, p, device=device)
 
+    def gpu_lcs(z, z1, z2, s, t):
+        handle.calls += 1
+        return lcs_solve(z, z1, z2, s, t, device=device)
+
     kernels.twed_band_serial = gpu_band
     kernels.twed_band_parallel = gpu_band
+    kernels.lcs_band_solve = gpu_lcs
     return handle

@@ -6,12 +6,13 @@ degree 1 and 2 (sqrt is IEEE-exact) and within 1e-12 relative for degree>=3
 (libm pow decides the last bits, pkg/src/twedband/_kernels.py:45-48).
 """
 
+import json
 import math
 
 import numpy as np
 import pytest
 
-from conftest import as_values, dec, same_float
+from conftest import GOLDEN, as_values, dec, same_float
 from paper_2007_16135_b200.workloads import make_pair, make_set
 
 
@@ -109,3 +110,26 @@ def test_oracle_is_not_product():
     for f in pkg.rglob("*.py"):
         text = f.read_text()
         assert "import oracle" not in text and "from oracle" not in text, f
+
+
+# ---- LCS: the oracle against the reference's values ----
+def lcs_golden():
+    return json.loads((GOLDEN / "lcs.json").read_text())
+
+
+def lcs_case(g):
+    rng = np.random.default_rng(g["seed"])
+    al = np.array(list(g["alphabet"]))
+    return "".join(rng.choice(al, size=g["ns"])), "".join(rng.choice(al, size=g["nt"]))
+
+
+def test_lcs_oracle_matches_reference_goldens():
+    from oracle import oracle as orc
+    gold = lcs_golden()
+    for c in gold["fixed"]:
+        assert orc.lcs(c["s"], c["t"]) == c["value"], c
+    for g in gold["generated"]:
+        s, t = lcs_case(g)
+        assert orc.lcs(s, t) == g["value"], g
+    # generic hashable symbols share one code table (core.py:152-160, test_band.py:297)
+    assert orc.lcs([1, "x", (2, 3), 4], ["x", (2, 3), 9]) == 2
