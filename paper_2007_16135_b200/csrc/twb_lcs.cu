@@ -41,7 +41,6 @@ namespace {
 
 using namespace twb;
 
-constexpr int LCS_KW = 2;  // 64-bit words per lane
 
 struct LcsArgs {
     const int32_t* s;        // row symbols, dense codes in [0, A) or -1 (absent from t)
@@ -49,8 +48,10 @@ struct LcsArgs {
     const uint64_t* pm;      // PM[c * W + w]
     int64_t W;               // words over the columns
     int64_t nt;              // columns
-    unsigned* carry;         // (G + 1) inboxes of ceil(ns / 32) packed carry words
-    long long* prog;         // G + 1 progress counters (carry words published)
+    // (G + 1) inboxes of ceil(ns / 32) slots: slot k = (k + 1) << 32 | the 32
+    // carry bits of rows 32k .. 32k+31 -- tag and payload in one 64-bit store,
+    // so the consumer polls the slot itself and no fence is needed
+    unsigned long long* carry;
     unsigned long long* ones;
 };
 
@@ -67,93 +68,146 @@ __global__ void lcs_masks_kernel(const int32_t* __restrict__ t, int64_t nt, int6
     }
 }
 
-__device__ __forceinline__ long long lcs_ld_acquire(const long long* p) {
-    long long v;
-    asm volatile("ld.acquire.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned long long lcs_ld_relaxed(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void lcs_st_release(long long* p, long long v) {
-    asm volatile("st.release.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void lcs_st_pred(unsigned long long* p, unsigned long long v, bool pred) {
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+                 "@q st.relaxed.gpu.global.u64 [%0], %1;\n\t}" ::"l"(p), "l"(v), "r"((int)pred)
+                 : "memory");
 }
 
-// V + U + cin over two 64-bit words (one carry chain); returns the carry out.
-__device__ __forceinline__ unsigned add2(uint64_t (&S)[2], const uint64_t (&V)[2],
-                                         const uint64_t (&U)[2], unsigned cin) {
-    unsigned s0l, s0h, s1l, s1h, co;
-    asm("{\n\t.reg .u32 t;\n\t"
-        "add.cc.u32 t, %5, 0xffffffff;\n\t"  // carry flag = cin (0 or 1)
-        "addc.cc.u32 %0, %6, %10;\n\t"
-        "addc.cc.u32 %1, %7, %11;\n\t"
-        "addc.cc.u32 %2, %8, %12;\n\t"
-        "addc.cc.u32 %3, %9, %13;\n\t"
-        "addc.u32 %4, 0, 0;\n\t}"
-        : "=r"(s0l), "=r"(s0h), "=r"(s1l), "=r"(s1h), "=r"(co)
-        : "r"(cin), "r"((unsigned)V[0]), "r"((unsigned)(V[0] >> 32)), "r"((unsigned)V[1]),
-          "r"((unsigned)(V[1] >> 32)), "r"((unsigned)U[0]), "r"((unsigned)(U[0] >> 32)),
-          "r"((unsigned)U[1]), "r"((unsigned)(U[1] >> 32)));
-    S[0] = ((uint64_t)s0h << 32) | s0l;
-    S[1] = ((uint64_t)s1h << 32) | s1l;
+// V + U + cin over KW 64-bit words (one carry chain); returns the carry out.
+template <int KW>
+__device__ __forceinline__ unsigned add_chain(uint64_t (&S)[KW], const uint64_t (&V)[KW],
+                                              const uint64_t (&U)[KW], unsigned cin) {
+    unsigned co;
+    if constexpr (KW == 1) {
+        unsigned sl, sh;
+        asm("{\n\t.reg .u32 t;\n\t"
+            "add.cc.u32 t, %3, 0xffffffff;\n\t"  // carry flag = cin (0 or 1)
+            "addc.cc.u32 %0, %4, %6;\n\t"
+            "addc.cc.u32 %1, %5, %7;\n\t"
+            "addc.u32 %2, 0, 0;\n\t}"
+            : "=r"(sl), "=r"(sh), "=r"(co)
+            : "r"(cin), "r"((unsigned)V[0]), "r"((unsigned)(V[0] >> 32)), "r"((unsigned)U[0]),
+              "r"((unsigned)(U[0] >> 32)));
+        S[0] = ((uint64_t)sh << 32) | sl;
+    } else {
+        static_assert(KW == 2, "one or two words per lane");
+        unsigned s0l, s0h, s1l, s1h;
+        asm("{\n\t.reg .u32 t;\n\t"
+            "add.cc.u32 t, %5, 0xffffffff;\n\t"
+            "addc.cc.u32 %0, %6, %10;\n\t"
+            "addc.cc.u32 %1, %7, %11;\n\t"
+            "addc.cc.u32 %2, %8, %12;\n\t"
+            "addc.cc.u32 %3, %9, %13;\n\t"
+            "addc.u32 %4, 0, 0;\n\t}"
+            : "=r"(s0l), "=r"(s0h), "=r"(s1l), "=r"(s1h), "=r"(co)
+            : "r"(cin), "r"((unsigned)V[0]), "r"((unsigned)(V[0] >> 32)), "r"((unsigned)V[1]),
+              "r"((unsigned)(V[1] >> 32)), "r"((unsigned)U[0]), "r"((unsigned)(U[0] >> 32)),
+              "r"((unsigned)U[1]), "r"((unsigned)(U[1] >> 32)));
+        S[0] = ((uint64_t)s0h << 32) | s0l;
+        S[1] = ((uint64_t)s1h << 32) | s1l;
+    }
     return co;
 }
 
-__global__ void __launch_bounds__(32) lcs_kernel(const LcsArgs a) {
-    static_assert(LCS_KW == 2, "add2 chains two words");
+// One warp per CTA. Steps run in chunks of 32: at a chunk's start the warp
+// stages the symbols of the rows its lanes meet in the chunk (rows outside
+// [0, ns) get the code of an all-zero mask, which makes them no-ops: with
+// M = 0 and carry-in 0, V and the carry out are unchanged), lane 0 fetches the
+// chunk's 32 carry bits from the previous CTA, and the 32 unrolled steps run
+// without a branch: mask lookup, carry by shuffle, add chain, update. Lane 31
+// publishes its 32 carry-outs of a word at step 30 of the next chunk.
+// SPM: the warp's slice of the masks ([A + 1][KW][32 lanes], last row zero)
+// lives in shared memory, else it is read through the read-only cache.
+template <int KW, bool SPM>
+__global__ void __launch_bounds__(32) lcs_kernel(const LcsArgs a, int alphabet) {
+    extern __shared__ uint64_t spm[];
+    __shared__ int ssym[64];
     const int lane = threadIdx.x;
     const int b = blockIdx.x;
     const int G = gridDim.x;
-    const int64_t w0 = ((int64_t)b * 32 + lane) * LCS_KW;
+    const int64_t w0 = ((int64_t)b * 32 + lane) * KW;
     const int64_t nwc = (a.ns + 31) / 32;  // carry words per inbox
-    const unsigned* cin_src = a.carry + (int64_t)b * nwc;
-    unsigned* cout_dst = a.carry + (int64_t)(b + 1) * nwc;
-    bool wok[LCS_KW];
-    uint64_t V[LCS_KW];
+    const unsigned long long* cin_src = a.carry + (int64_t)b * nwc;
+    unsigned long long* cout_dst = a.carry + (int64_t)(b + 1) * nwc;
+    bool wok[KW];
+    uint64_t V[KW];
 #pragma unroll
-    for (int k = 0; k < LCS_KW; ++k) {
+    for (int k = 0; k < KW; ++k) {
         wok[k] = w0 + k < a.W;
         V[k] = ~0ull;
     }
-    unsigned cout_prev = 0, cin_word = 0, cpack = 0;
-    const int64_t nsteps = a.ns + 31;
-    for (int64_t st = 0; st < nsteps; ++st) {
-        const int64_t i = st - lane;  // this lane's row
-        unsigned cin = __shfl_up_sync(0xffffffffu, cout_prev, 1);
-        if (lane == 0) {
-            cin = 0;
-            if (b > 0 && st < a.ns) {
-                if ((st & 31) == 0) {  // the next 32 rows' carries from CTA b-1
-                    while (lcs_ld_acquire(a.prog + b) < (st >> 5) + 1) __nanosleep(32);
-                    cin_word = __ldcg(cin_src + (st >> 5));
-                }
-                cin = (cin_word >> (st & 31)) & 1u;
-            }
-        }
-        unsigned co = 0;
-        if (i >= 0 && i < a.ns) {
-            const int sym = __ldg(a.s + i);
-            uint64_t M[LCS_KW], U[LCS_KW], S[LCS_KW];
+    if constexpr (SPM) {
+        for (int c = 0; c <= alphabet; ++c)
 #pragma unroll
-            for (int k = 0; k < LCS_KW; ++k) {
-                M[k] = (sym >= 0 && wok[k]) ? __ldg(a.pm + (int64_t)sym * a.W + w0 + k) : 0ull;
+            for (int k = 0; k < KW; ++k)
+                spm[((int64_t)c * KW + k) * 32 + lane] =
+                    (c < alphabet && wok[k]) ? __ldg(a.pm + (int64_t)c * a.W + w0 + k) : 0ull;
+    }
+    unsigned co = 0, cp = 0;
+    // symbols of rows st0 - 31 .. st0 + 32 (two per lane), loaded one chunk ahead
+    auto fetch_syms = [&](int64_t st0, int (&c)[2]) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t r = st0 - 31 + h * 32 + lane;
+            c[h] = (r >= 0 && r < a.ns) ? __ldg(a.s + r) : -1;
+        }
+    };
+    int nxt[2];
+    fetch_syms(0, nxt);
+    for (int64_t st0 = 0; st0 <= 32 * nwc; st0 += 32) {
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; ++h)  // -1 (cannot match, or no row) -> the zero mask
+            ssym[h * 32 + lane] = nxt[h] < 0 ? alphabet : nxt[h];
+        fetch_syms(st0 + 32, nxt);
+        unsigned cwin = 0;  // carries into rows st0 .. st0 + 31 (used by lane 0)
+        if (b > 0 && st0 < a.ns) {  // warp-uniform: every lane polls the same slot
+            const unsigned long long tag = (unsigned long long)((st0 >> 5) + 1) << 32;
+            unsigned long long v;
+            while (((v = lcs_ld_relaxed(cin_src + (st0 >> 5))) >> 32 << 32) != tag) __nanosleep(20);
+            cwin = (unsigned)v;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const int sym = ssym[j - lane + 31];
+            uint64_t M[KW], U[KW], S[KW];
+#pragma unroll
+            for (int k = 0; k < KW; ++k) {
+                if constexpr (SPM) M[k] = spm[((int64_t)sym * KW + k) * 32 + lane];
+                else M[k] = (sym < alphabet && wok[k]) ? __ldg(a.pm + (int64_t)sym * a.W + w0 + k) : 0ull;
                 U[k] = V[k] & M[k];
             }
-            co = add2(S, V, U, cin);
+            unsigned cin = __shfl_up_sync(0xffffffffu, co, 1);
+            cin = lane == 0 ? (cwin >> j) & 1u : cin;
+            co = add_chain<KW>(S, V, U, cin);
 #pragma unroll
-            for (int k = 0; k < LCS_KW; ++k) V[k] = S[k] | (V[k] & ~M[k]);
-            if (lane == 31 && b + 1 < G) {
-                cpack |= co << (i & 31);
-                if ((i & 31) == 31 || i == a.ns - 1) {
-                    cout_dst[i >> 5] = cpack;
-                    cpack = 0;
-                    lcs_st_release(a.prog + b + 1, (i >> 5) + 1);
+            for (int k = 0; k < KW; ++k) V[k] = S[k] | (V[k] & ~M[k]);
+            // lane 31 met row st0 + j - 31: bit (j + 1) & 31 of word ((st0 + j - 31) >> 5)
+            if (j == 31) {
+                cp = co;
+            } else {
+                cp |= co << (j + 1);
+                if (j == 30) {  // word (st0 >> 5) - 1 complete
+                    const int64_t wd = (st0 >> 5) - 1;
+                    // predicated, not branched: a divergent region here would
+                    // make every shuffle of the chunk a WARPSYNC.COLLECTIVE
+                    lcs_st_pred(cout_dst + (wd < 0 ? 0 : wd), (unsigned long long)(wd + 1) << 32 | cp,
+                                lane == 31 && b + 1 < G && wd >= 0 && wd < nwc);
                 }
             }
         }
-        cout_prev = co;
     }
     // columns still set in V are not in the LCS
     unsigned long long ones = 0;
 #pragma unroll
-    for (int k = 0; k < LCS_KW; ++k) {
+    for (int k = 0; k < KW; ++k) {
         if (!wok[k]) continue;
         uint64_t v = V[k];
         const int64_t w = w0 + k;
@@ -191,22 +245,49 @@ extern "C" int twb_lcs_i32(const int32_t* s, int64_t ns, const int32_t* t, int64
         std::swap(ns, nt);
     }
     const int64_t W = (nt + 63) / 64;
-    const int64_t G = (W + 32 * LCS_KW - 1) / (32 * LCS_KW);
     if ((double)alphabet * (double)W * 8.0 > 4.0e9)
         return api_fail(TWB_EUNSUP, "alphabet x length too large for the match-mask table (> 4 GB)");
     cudaStream_t st = cudaStreamPerThread;
-    void *d_s = nullptr, *d_t = nullptr, *d_pm = nullptr, *d_carry = nullptr, *d_prog = nullptr,
-         *d_ones = nullptr;
+    void *d_s = nullptr, *d_t = nullptr, *d_pm = nullptr, *d_carry = nullptr, *d_ones = nullptr;
     auto cleanup = [&]() {
-        for (void* p : {d_s, d_t, d_pm, d_carry, d_prog, d_ones})
+        for (void* p : {d_s, d_t, d_pm, d_carry, d_ones})
             if (p) cudaFreeAsync(p, st);
         cudaStreamSynchronize(st);
     };
     LCK(cudaSetDevice(device));
-    int sms = 0, occ = 0;
+    int sms = 0;
     LCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    LCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lcs_kernel, 32, 0));
-    if (G > (int64_t)sms * occ) {
+    // The widest variant whose grid is co-resident: one word per lane (the
+    // shortest carry chain per step), masks in shared memory when they fit.
+    using Kern = void (*)(const LcsArgs, int);
+    struct Cand {
+        Kern k;
+        int kw;
+        bool spm;
+    };
+    const Cand cands[] = {{lcs_kernel<1, true>, 1, true}, {lcs_kernel<1, false>, 1, false},
+                          {lcs_kernel<2, true>, 2, true}, {lcs_kernel<2, false>, 2, false}};
+    Kern kern = nullptr;
+    int64_t G = 0;
+    size_t smem = 0;
+    for (const Cand& c : cands) {
+        const size_t sm = c.spm ? (size_t)(alphabet + 1) * c.kw * 32 * sizeof(uint64_t) : 0;
+        if (sm > 200 * 1024) continue;
+        if (cudaFuncSetAttribute(c.k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        int occ = 0;
+        LCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, c.k, 32, sm));
+        const int64_t g = (W + 32 * c.kw - 1) / (32 * c.kw);
+        if (occ > 0 && g <= (int64_t)sms * occ) {
+            kern = c.k;
+            G = g;
+            smem = sm;
+            break;
+        }
+    }
+    if (!kern) {
         cleanup();
         return api_fail(TWB_EUNSUP, "sequence too long for one co-resident sweep");
     }
@@ -214,25 +295,25 @@ extern "C" int twb_lcs_i32(const int32_t* s, int64_t ns, const int32_t* t, int64
     LCK(cudaMallocAsync(&d_s, sizeof(int32_t) * ns, st));
     LCK(cudaMallocAsync(&d_t, sizeof(int32_t) * nt, st));
     LCK(cudaMallocAsync(&d_pm, sizeof(uint64_t) * (size_t)alphabet * W, st));
-    LCK(cudaMallocAsync(&d_carry, sizeof(unsigned) * (size_t)(G + 1) * nwc, st));
-    LCK(cudaMallocAsync(&d_prog, sizeof(long long) * (G + 1), st));
+    LCK(cudaMallocAsync(&d_carry, sizeof(unsigned long long) * (size_t)(G + 1) * nwc, st));
     LCK(cudaMallocAsync(&d_ones, sizeof(unsigned long long), st));
     LCK(cudaMemcpyAsync(d_s, s, sizeof(int32_t) * ns, cudaMemcpyHostToDevice, st));
     LCK(cudaMemcpyAsync(d_t, t, sizeof(int32_t) * nt, cudaMemcpyHostToDevice, st));
     LCK(cudaMemsetAsync(d_pm, 0, sizeof(uint64_t) * (size_t)alphabet * W, st));
-    LCK(cudaMemsetAsync(d_prog, 0, sizeof(long long) * (G + 1), st));
+    LCK(cudaMemsetAsync(d_carry, 0, sizeof(unsigned long long) * (size_t)(G + 1) * nwc, st));
     LCK(cudaMemsetAsync(d_ones, 0, sizeof(unsigned long long), st));
     lcs_masks_kernel<<<(unsigned)((W + 255) / 256), 256, 0, st>>>((const int32_t*)d_t, nt, W,
                                                                  (uint64_t*)d_pm);
     api_count_launch();
     LCK(cudaGetLastError());
-    LcsArgs a{(const int32_t*)d_s, ns, (const uint64_t*)d_pm, W, nt, (unsigned*)d_carry,
-              (long long*)d_prog, (unsigned long long*)d_ones};
-    void* params[] = {(void*)&a};
+    LcsArgs a{(const int32_t*)d_s, ns, (const uint64_t*)d_pm, W, nt,
+              (unsigned long long*)d_carry, (unsigned long long*)d_ones};
+    int alpha = alphabet;
+    void* params[] = {(void*)&a, (void*)&alpha};
     LaunchCtx* ctx = api_ctx_begin();
     ctx->before(st);
     // cooperative: CTA b spins on CTA b-1, all must be resident
-    LCK(cudaLaunchCooperativeKernel((const void*)lcs_kernel, dim3((unsigned)G), dim3(32), params, 0,
+    LCK(cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)G), dim3(32), params, smem,
                                     st));
     ctx->after(st);
     unsigned long long ones = 0;
