@@ -446,6 +446,7 @@ def run_extra(args, world, rank, local):
         kms = max_over_ranks(float(np.median(ks)), world)
         res[name] = {"n": wl["n"], "d": wl["d"], "dtype": wl["dtype"], "kernel_ms": kms,
                      "gcups": wl["n"] * wl["n"] / (kms * 1e-3) / 1e9, "result": out.item()}
+    res["lcs"] = run_lcs(args, world, rank)
     # cfg4: AA 1000 x 256 (seed 3) against BB 1000 x 256 (seed 4), d = 1, fp64, full
     AA, TAA = make_set(1000, 256, 1, 3)
     BB, TBB = make_set(1000, 256, 1, 4)
@@ -466,6 +467,44 @@ def run_extra(args, world, rank, local):
                    "gcups": 1e6 * 256 * 256 / (kms * 1e-3) / 1e9, "n_gpus": world,
                    "sharding": "rows, no collective in the timed kernel"}
     return res
+
+
+def run_lcs(args, world, rank):
+    """LCS length of two random DNA strings of 1M symbols:
+    the bit-parallel kernel's event time (twb_lcs_i32), and on rank 0 of a 1-GPU
+    run the reference's own lcs_band (numba three-diagonal band, one thread) on a
+    bounded 20k x 20k sample of the same generator."""
+    from paper_2007_16135_b200 import _lib
+    from paper_2007_16135_b200.api import lcs_codes
+
+    lib = _lib.load()
+    lib.twb_set_kernel_timing(1)
+    n = 1_000_000
+    rng = np.random.default_rng(2007)
+    a = rng.integers(0, 4, n)
+    b = rng.integers(0, 4, n)
+    lcs_codes(a[:4096], b[:4096])
+    ks = []
+    for _ in range(3):
+        r = lcs_codes(a, b)
+        ks.append(lib.twb_last_kernel_ms())
+    kms = max_over_ranks(float(min(ks)), world)
+    out = {"n": n, "alphabet": 4, "kernel_ms": kms, "gcups": n * n / (kms * 1e-3) / 1e9,
+           "result": r, "kernel": "lcs_kernel (bit-parallel, 64 cells per word op)"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        tb = load_reference()
+        if tb is not None:
+            m = 20_000
+            sa = "".join("ACGT"[x] for x in a[:m])
+            sb = "".join("ACGT"[x] for x in b[:m])
+            tb.lcs_band(sa[:500], sb[:500])  # JIT
+            t0 = time.perf_counter()
+            rv = tb.lcs_band(sa, sb)
+            dt = time.perf_counter() - t0
+            assert rv == lcs_codes(a[:m], b[:m])
+            out["cpu_reference"] = {"gcups": m * m / dt / 1e9, "seconds": dt, "sample": f"{m} x {m}",
+                                    "what": "twedband.lcs_band (numba band, 1 thread)"}
+    return out
 
 
 def run_pair_all_gpus(args, world, rank, host):
