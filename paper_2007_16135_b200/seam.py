@@ -81,7 +81,9 @@ def install(twedband_module=None, device=0) -> Installed:
         import twedband as twedband_module  # the reference package
     kernels = twedband_module._kernels
     _lib.require_device()
-    names = ("twed_band_serial", "twed_band_parallel", "lcs_band_solve")
+    names = ("twed_band_serial", "twed_band_parallel")
+    if hasattr(kernels, "lcs_band_solve"):  # present in the reference; optional here
+        names += ("lcs_band_solve",)
     saved = {name: getattr(kernels, name) for name in names}
     handle = Installed(kernels, saved)
 
@@ -95,5 +97,6 @@ def install(twedband_module=None, device=0) -> Installed:
 
     kernels.twed_band_serial = gpu_band
     kernels.twed_band_parallel = gpu_band
-    kernels.lcs_band_solve = gpu_lcs
+    if "lcs_band_solve" in saved:
+        kernels.lcs_band_solve = gpu_lcs
     return handle
