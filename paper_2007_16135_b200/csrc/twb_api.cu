@@ -259,8 +259,6 @@ int twed_pair_dev(const T* dA, int64_t nA, const T* dTA, const T* dB, int64_t nB
     check_unsafe(dTA, nA, lim, dflag, st);
     check_unsafe(dB, nB * dim, lim, dflag, st, safe_tiny<R>());
     check_unsafe(dTB, nB, lim, dflag, st);
-    int hflag = 0;
-    CK(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
 
     R* V[2] = {sc.get_n<R>((nA + 1) * dim), sc.get_n<R>((nB + 1) * dim)};
     R* Tm[2] = {sc.get_n<R>(nA + 1), sc.get_n<R>(nB + 1)};
@@ -274,28 +272,43 @@ int twed_pair_dev(const T* dA, int64_t nA, const T* dTA, const T* dB, int64_t nB
     if ((rc = prepare<T, R, Z>(dB, dTB, nullptr, 1, nB, nB, dim, nu, lam, degree, V[1], Tm[1],
                                Del[1], st)))
         return rc;
-    CK(cudaStreamSynchronize(st));  // hflag
-    Variant v = pick_variant(dim, degree, nu, lam, hflag != 0, lim);
-    // Rows = the longer series (more stripes for the SMs). Exact symmetry
-    // twed(a,b) == twed(b,a) makes the swap bit-identical when the min is
-    // order-free (not in the NaN-exact mode).
-    int ra = 0, rb = 1;
-    int64_t na = nA, nb = nB;
-    if (!v.E && nB > nA && !getenv("TWB_NO_SWAP")) {  // env: tuning experiments
-        ra = 1;
-        rb = 0;
-        std::swap(na, nb);
+    // No host round trip: the data-dependent choice between the proven-safe
+    // sweep and the NaN-exact one is made on the device. Both are launched,
+    // gated on the check's flag; the one not wanted returns at once. The call
+    // stays asynchronous on the caller's stream (and capturable in a CUDA
+    // graph). The safe sweep goes last so kernel timing brackets it.
+    auto sweep = [&](const Variant& v, const int* gate, int want) -> int {
+        // Rows = the longer series (more stripes for the SMs). Exact symmetry
+        // twed(a,b) == twed(b,a) makes the swap bit-identical when the min is
+        // order-free (not in the NaN-exact mode).
+        int ra = 0, rb = 1;
+        int64_t na = nA, nb = nB;
+        if (!v.E && nB > nA && !getenv("TWB_NO_SWAP")) {  // env: tuning experiments
+            ra = 1;
+            rb = 0;
+            std::swap(na, nb);
+        }
+        WaveProblem<R, Z> pr;
+        pr.A = {V[ra], Tm[ra], Del[ra]};
+        pr.B = {V[rb], Tm[rb], Del[rb]};
+        pr.nA = na;
+        pr.nB = nb;
+        pr.nu = nu;
+        pr.p = degree;
+        pr.out = zout;
+        pr.gate = gate;
+        pr.gate_want = want;
+        CK(call_wave<R, Z>(dim, v.P, v.E, v.N1, pr, sc, st));
+        if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
+        return 0;
+    };
+    const Variant v_safe = pick_variant(dim, degree, nu, lam, false, lim);
+    if (v_safe.E) {  // parameters alone rule the safe sweep out
+        if ((rc = sweep(v_safe, nullptr, 0))) return rc;
+    } else {
+        if ((rc = sweep(pick_variant(dim, degree, nu, lam, true, lim), dflag, 1))) return rc;
+        if ((rc = sweep(v_safe, dflag, 0))) return rc;
     }
-    WaveProblem<R, Z> pr;
-    pr.A = {V[ra], Tm[ra], Del[ra]};
-    pr.B = {V[rb], Tm[rb], Del[rb]};
-    pr.nA = na;
-    pr.nB = nb;
-    pr.nu = nu;
-    pr.p = degree;
-    pr.out = zout;
-    CK(call_wave<R, Z>(dim, v.P, v.E, v.N1, pr, sc, st));
-    if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
     static_assert(sizeof(Z) == 8, "pairs accumulate in fp64");
     CK(cudaMemcpyAsync(d_out, zout, sizeof(double), cudaMemcpyDeviceToDevice, st));
     return 0;

@@ -420,6 +420,8 @@ struct WaveArgs {
     int p;
     double* out;
     long long* dbg;  // diagnostics (TWB_DBG_TIMES): per stripe start / input ready / end (ns)
+    const int* gate;  // run only if (*gate & 1) == gate_want (device-side variant choice)
+    int gate_want;
 };
 
 __device__ __forceinline__ long long globaltimer() {
@@ -455,6 +457,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
     R* srows = reinterpret_cast<R*>(smem_raw + wave_smem_base<D, R, Z, C>(WARPS));  // SA rows (16-aligned)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    if (args.gate && ((__ldcg(args.gate) & 1) != args.gate_want)) return;  // the other variant runs
     const int G = gridDim.x;
     const int b = blockIdx.x;
     const int64_t gb = args.cta0 + b;  // ring position

@@ -71,6 +71,8 @@ struct WaveProblem {
     int p;
     Z* out;  // device, one value
     CtaRing<R, Z>* ring = nullptr;  // multi-kernel ring (A, B, out, alloc, st per part)
+    const int* gate = nullptr;      // device flag: run only if (*gate & 1) == gate_want
+    int gate_want = 0;
 };
 
 // Batch kernel variants (lanes per series LW, rows per lane K): row-side
@@ -237,6 +239,8 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
         a.abort = nl > 1 ? pr.ring->abort : nullptr;
         a.timeout_ns = pr.ring ? pr.ring->timeout_ns : 0;
         a.dbg = nullptr;
+        a.gate = pr.gate;
+        a.gate_want = pr.gate_want;
     }
     for (int l = 0; l < nl; ++l) {  // the last CTA of each part feeds the next part's CTA 0
         const WaveArgs<R, Z>& nx = args[(l + 1) % nl];

@@ -288,3 +288,30 @@ def test_validation_messages(twb):
         twb.twed([1.0, 2.0], [1.0, 1.0], [1.0], [0.0])
     with pytest.raises(twb.InvalidInputError):
         twb.twed_batch([np.array([1.0])], None, [np.array([2.0])], None, tri=True)
+
+
+def test_device_api_is_async_and_graph_capturable(twb):
+    """twed_dev makes the safe / NaN-exact choice on the device (no host round
+    trip), so it can be captured in a CUDA graph and replayed on new data."""
+    import torch
+    from paper_2007_16135_b200.workloads import make_pair
+    dev = torch.device("cuda:0")
+    a, ta, b, tb = make_pair(3000, 3, 31)
+    t = [torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in (a, ta, b, tb)]
+    out = torch.empty(1, dtype=torch.float64, device=dev)
+    twb.twed_dev(*t, nu=1.0, lamb=1.0, degree=2, out=out)  # warm (kernel attributes)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        twb.twed_dev(*t, nu=1.0, lamb=1.0, degree=2, out=out)
+    for seed in (32, 33):
+        a2, ta2, b2, tb2 = make_pair(3000, 3, seed)
+        if seed == 33:
+            a2[1234, 1] = np.nan  # the captured graph takes the NaN-exact sweep
+        for dst, src in zip(t, (a2, ta2, b2, tb2)):
+            dst.copy_(torch.from_numpy(np.ascontiguousarray(src)))
+        g.replay()
+        torch.cuda.synchronize()
+        want = twb.twed(a2, ta2, b2, tb2, 1.0, 1.0, 2)
+        got = out.item()
+        assert (math.isnan(want) and math.isnan(got)) or got == want, (seed, got, want)
