@@ -124,6 +124,9 @@ __global__ void prepare_kernel(const T* __restrict__ values, const T* __restrict
 // Batch: all-pairs matrix.
 // ---------------------------------------------------------------------------
 constexpr int MAX_CHUNK = 64;  // B series per task
+#ifndef TWB_BATCH_ALLEND  // 1: every lane runs the series-end bookkeeping (A/B only)
+#define TWB_BATCH_ALLEND 0
+#endif
 
 template <int D, typename R, typename Z>
 __host__ __device__ constexpr size_t batch_smem(int warps) {
@@ -309,7 +312,10 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
                         const R tbn = ring.t[slot];
                         L.prep(mn, tbn, ring.del[slot], zpn, mup, tbj, args.nu, pre);
                         tbj = tbn;
-                        if (++pos == curlen) series_end(j);
+                        // only lane 0 (col0 of the next series) and the writer (the result) need
+                        // the series bookkeeping: other lanes skip it, so a series end is a
+                        // divergent step for two lanes instead of all 32
+                        if (++pos == curlen && (TWB_BATCH_ALLEND || hl == 0 || writer)) series_end(j);
                     }
                 };
                 while (s + 16 <= ncols) {  // lanes' columns s - hl .. s + 15 - hl all valid
