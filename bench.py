@@ -446,7 +446,7 @@ def run_extra(args, world, rank, local):
         kms = max_over_ranks(float(np.median(ks)), world)
         res[name] = {"n": wl["n"], "d": wl["d"], "dtype": wl["dtype"], "kernel_ms": kms,
                      "gcups": wl["n"] * wl["n"] / (kms * 1e-3) / 1e9, "result": out.item()}
-    res["lcs"] = run_lcs(args, world, rank)
+    res["lcs"] = run_lcs(args, world, rank, local)
     # cfg4: AA 1000 x 256 (seed 3) against BB 1000 x 256 (seed 4), d = 1, fp64, full
     AA, TAA = make_set(1000, 256, 1, 3)
     BB, TBB = make_set(1000, 256, 1, 4)
@@ -469,7 +469,7 @@ def run_extra(args, world, rank, local):
     return res
 
 
-def run_lcs(args, world, rank):
+def run_lcs(args, world, rank, local):
     """LCS length of two random DNA strings of 1M symbols:
     the bit-parallel kernel's event time (twb_lcs_i32), and on rank 0 of a 1-GPU
     run the reference's own lcs_band (numba three-diagonal band, one thread) on a
@@ -483,10 +483,10 @@ def run_lcs(args, world, rank):
     rng = np.random.default_rng(2007)
     a = rng.integers(0, 4, n)
     b = rng.integers(0, 4, n)
-    lcs_codes(a[:4096], b[:4096])
+    lcs_codes(a[:4096], b[:4096], device=local)
     ks = []
     for _ in range(3):
-        r = lcs_codes(a, b)
+        r = lcs_codes(a, b, device=local)
         ks.append(lib.twb_last_kernel_ms())
     kms = max_over_ranks(float(min(ks)), world)
     out = {"n": n, "alphabet": 4, "kernel_ms": kms, "gcups": n * n / (kms * 1e-3) / 1e9,
@@ -501,7 +501,7 @@ def run_lcs(args, world, rank):
             t0 = time.perf_counter()
             rv = tb.lcs_band(sa, sb)
             dt = time.perf_counter() - t0
-            assert rv == lcs_codes(a[:m], b[:m])
+            assert rv == lcs_codes(a[:m], b[:m], device=local)
             out["cpu_reference"] = {"gcups": m * m / dt / 1e9, "seconds": dt, "sample": f"{m} x {m}",
                                     "what": "twedband.lcs_band (numba band, 1 thread)"}
     return out

@@ -45,6 +45,18 @@ int fail(int code, const char* fmt, ...) {
                         __LINE__);                                                             \
     } while (0)
 
+// Host entry points select their device; the caller's current device is put
+// back when the call returns (a library call must not move it).
+struct DeviceGuard {
+    int prev = -1;
+    DeviceGuard() {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 // Stream-ordered scratch, released (asynchronously) when the call returns.
 struct Scratch {
     cudaStream_t st;
@@ -320,6 +332,7 @@ int twed_pair_host(const T* A, int64_t nA, const T* TA, const T* B, int64_t nB, 
     int rc = check_params(nA, nB, dim, nu, lam, degree);
     if (rc) return rc;
     if (!A || !TA || !B || !TB || !out) return fail(TWB_EINVAL, "null pointer argument");
+    DeviceGuard device_guard;
     CK(cudaSetDevice(device));
     init_pool(device);
     cudaStream_t st = cudaStreamPerThread;
@@ -363,6 +376,7 @@ int twed_pair_multi(const T* A, int64_t nA, const T* TA, const T* B, int64_t nB,
     if (rc) return rc;
     if (!A || !TA || !B || !TB || !out || !devices) return fail(TWB_EINVAL, "null pointer argument");
     if (ndev < 1 || ndev > 64) return fail(TWB_EINVAL, "ndev must be in [1, 64], got %d", ndev);
+    DeviceGuard device_guard;
     int count = 0;
     CK(cudaGetDeviceCount(&count));
     for (int q = 0; q < ndev; ++q)
@@ -743,6 +757,7 @@ int twed_batch_host(const T* AA, const int64_t* a_off, int64_t nAA, const T* TAA
                          row_end);
     if (rc) return rc;
     if (!AA || !TAA || !out || (!self && (!TBB || !b_off))) return fail(TWB_EINVAL, "null pointer argument");
+    DeviceGuard device_guard;
     CK(cudaSetDevice(device));
     init_pool(device);
     cudaStream_t st = cudaStreamPerThread;
@@ -855,6 +870,7 @@ extern "C" {
 
 int64_t twb_selftest_sqrt(int64_t n, uint64_t seed, int32_t device, int64_t* fast_count) {
     if (n < 1) return fail(TWB_EINVAL, "n must be >= 1");
+    DeviceGuard device_guard;
     CK(cudaSetDevice(device));
     cudaStream_t st = cudaStreamPerThread;
     unsigned long long* d = nullptr;
@@ -872,6 +888,7 @@ int64_t twb_selftest_sqrt(int64_t n, uint64_t seed, int32_t device, int64_t* fas
 }
 
 double twb_probe_add_rate(int fp64, int device) {
+    DeviceGuard device_guard;
     if (cudaSetDevice(device) != cudaSuccess) return -1.0;
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
@@ -1027,6 +1044,7 @@ int twb_band_solve_f64(const double* va, const double* ta, const double* dela, i
     int rc = check_params(na, nb, dim, nu, 0.0, degree);
     if (rc) return rc;
     if (!va || !ta || !dela || !vb || !tb || !delb || !out) return fail(TWB_EINVAL, "null pointer argument");
+    DeviceGuard device_guard;
     CK(cudaSetDevice(device));
     init_pool(device);
     cudaStream_t st = cudaStreamPerThread;
@@ -1080,6 +1098,7 @@ int twb_prepare_series_f64(const double* values, const double* times, int64_t n,
                            double nu, double lam, int32_t degree, int32_t device, double* ext_values,
                            double* ext_times, double* deletion) {
     if (n < 1 || dim < 1 || degree < 1) return fail(TWB_EINVAL, "bad series");
+    DeviceGuard device_guard;
     CK(cudaSetDevice(device));
     init_pool(device);
     cudaStream_t st = cudaStreamPerThread;

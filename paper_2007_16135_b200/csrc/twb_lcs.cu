@@ -254,6 +254,14 @@ extern "C" int twb_lcs_i32(const int32_t* s, int64_t ns, const int32_t* t, int64
             if (p) cudaFreeAsync(p, st);
         cudaStreamSynchronize(st);
     };
+    int prev_dev = -1;
+    if (cudaGetDevice(&prev_dev) != cudaSuccess) prev_dev = -1;
+    struct Restore {
+        int d;
+        ~Restore() {
+            if (d >= 0) cudaSetDevice(d);
+        }
+    } restore{prev_dev};
     LCK(cudaSetDevice(device));
     int sms = 0;
     LCK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
