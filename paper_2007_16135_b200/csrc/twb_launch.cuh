@@ -323,7 +323,24 @@ cudaError_t run_wave(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream
     // 395 GCUPS vs 376 for 8 x 8, d = 1 920 vs 775, fp32 mode 874 vs 507).
     // Shorter: 4 rows per lane, stripes of up to 12 warps sized by the cost
     // model (n = 300k d = 3: 346 GCUPS; n = 100k: d = 1 331, d = 3 170).
-    if (pr.nA >= (int64_t)sms * 12 * 32 * 6 * 3 / 2)
+    const int64_t long_rows = (int64_t)sms * 12 * 32 * 6 * 3 / 2;  // 1.5 rounds of k6w12 (511k)
+    if constexpr (!E && sizeof(R) == 8) {
+        // fp64 mid sizes (B200 sweep, profiles/r01i_sweep_mid_sizes.log): the
+        // wavefront depth nA / K dominates, so taller lanes (8 rows) win once
+        // there are enough of them; short row sides keep more, shorter warps.
+        //   d >= 3: 100k 207 (k8w8) vs 200 (k6w12) vs 152 (k4w12) GCUPS; 300k 382 vs 333 vs 344;
+        //           600k 464 vs 415 vs 383; 1M 409 vs 484 vs 401; 30k 62 vs 58 vs 67
+        //   d = 1 : 100k 332 vs 357 vs 334; 300k 710 vs 679 vs 667
+        //   d = 2 : 100k  84 vs 238 vs 201; 300k 233 vs 366 vs 385
+        const int64_t n = pr.nA;
+        if (D >= 3 && n >= (int64_t)sms * 400 && n < (int64_t)sms * 5400)
+            return run_wave_cfg<D, 8, 1, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
+        if (D == 1 && n >= (int64_t)sms * 1350 && n < long_rows)
+            return run_wave_cfg<D, 8, 1, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
+        if (D <= 2 && n < (int64_t)sms * 1350 && n >= (int64_t)sms * 150)
+            return run_wave_cfg<D, 6, 1, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
+    }
+    if (pr.nA >= long_rows)
         return run_wave_cfg<D, 6, 1, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
     return run_wave_cfg<D, 4, 1, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
 }
