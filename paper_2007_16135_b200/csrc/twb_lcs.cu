@@ -12,16 +12,16 @@
 //
 // Layout and schedule. Columns are the longer sequence (more parallel width),
 // rows the shorter one (LCS is symmetric). The bit-vector is cut into 64-bit
-// words; lane l of CTA b (one warp per CTA) owns LCS_KW consecutive words and
-// keeps them in registers for the whole sweep. Rows stream by: at step st lane
-// l handles row st - l, so the carry out of its top word reaches lane l+1 by
-// warp shuffle exactly when that lane needs it (the same one-step lane skew as
-// the TWED wavefront). Lane 31's carries leave the CTA packed 32 rows per
-// word into the next CTA's inbox with a release-published progress counter;
-// lane 0 of the next CTA polls it with acquire once per 32 rows. The carry
-// chain over a lane's words is one add.cc/addc.cc sequence. Match masks
-// PM[c][w] are built once on the device (A x W x 8 bytes) and read through
-// the read-only cache.
+// words; lane l of CTA b (one warp per CTA) owns KW consecutive words (KW = 1
+// unless the grid would not be co-resident) and keeps them in registers for
+// the whole sweep. Rows stream by: at step st lane l handles row st - l, so
+// the carry out of its top word reaches lane l+1 by warp shuffle exactly when
+// that lane needs it (the same one-step lane skew as the TWED wavefront). Lane
+// 31's carries leave the CTA packed 32 rows per 64-bit slot, tagged with the
+// slot index in the same store; the next CTA polls the slot itself, loading it
+// one chunk of 32 rows ahead. The carry chain over a lane's words is one
+// add.cc/addc.cc sequence. Match masks PM[c][w] are built once on the device
+// (A x W x 8 bytes) and each warp keeps its slice in shared memory.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(32) lcs_kernel(const LcsArgs a, int alphabet) 
     };
     int nxt[2];
     fetch_syms(0, nxt);
+    unsigned long long cpre = b > 0 ? lcs_ld_relaxed(cin_src) : 0ull;  // next chunk's carry slot
     for (int64_t st0 = 0; st0 <= 32 * nwc; st0 += 32) {
         __syncwarp();
 #pragma unroll
@@ -168,10 +169,17 @@ __global__ void __launch_bounds__(32) lcs_kernel(const LcsArgs a, int alphabet) 
         fetch_syms(st0 + 32, nxt);
         unsigned cwin = 0;  // carries into rows st0 .. st0 + 31 (used by lane 0)
         if (b > 0 && st0 < a.ns) {  // warp-uniform: every lane polls the same slot
-            const unsigned long long tag = (unsigned long long)((st0 >> 5) + 1) << 32;
-            unsigned long long v;
-            while (((v = lcs_ld_relaxed(cin_src + (st0 >> 5))) >> 32 << 32) != tag) __nanosleep(20);
+            // the slot was loaded one chunk ago (its L2 latency hidden behind 32
+            // steps); reload only while the producer has not reached it
+            const int64_t k = st0 >> 5;
+            const unsigned long long tag = (unsigned long long)(k + 1) << 32;
+            unsigned long long v = cpre;
+            while ((v >> 32 << 32) != tag) {
+                __nanosleep(20);
+                v = lcs_ld_relaxed(cin_src + k);
+            }
             cwin = (unsigned)v;
+            if (k + 1 < nwc) cpre = lcs_ld_relaxed(cin_src + k + 1);
         }
         __syncwarp();
 #pragma unroll

@@ -24,9 +24,9 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu \
   > gpurun_out/${TAG}_ncu_launch_bench.log 2>&1
 echo "ncu launches exit $?" >> gpurun_out/${TAG}_ncu_launch_bench.log
-TWB_WAVE_CFG=k6w12 TWB_WAVE_WS=12 timeout 900 ncu --set full --clock-control none --import-source on -k regex:wave_kernel -c 1 \
+TWB_WAVE_CFG=k6w12 TWB_WAVE_WS=12 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:wave_kernel<.*\(bool\)0, \(bool\)[01], \(int\)' -c 1 \
   -o gpurun_out/${TAG}_wave_k6w12_n400k -f python scripts/prof_one.py cfg3 --n 400000 > gpurun_out/${TAG}_ncu_wave.log 2>&1
-timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none -k regex:wave_kernel -c 1 \
+timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --kernel-name-base demangled -k 'regex:wave_kernel<.*\(bool\)0, \(bool\)[01], \(int\)' -c 1 \
   --csv --log-file gpurun_out/${TAG}_wave_cfg3_dram.csv python scripts/prof_one.py cfg3 > gpurun_out/${TAG}_ncu_wave_dram.log 2>&1
 echo "ncu wave exit $?" >> gpurun_out/${TAG}_ncu_wave.log
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:batch_kernel -c 1 \
