@@ -25,6 +25,7 @@ fp32-rounded inputs).
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 
@@ -167,11 +168,60 @@ def batch_matrix(list_a, list_b, params: TwedParams, symmetric=False, device=0,
     f32 = va.dtype == np.float32
     out = np.empty((row_end - row_begin, nB), dtype=np.float32 if f32 else np.float64)
     fn = lib.twb_twed_batch_f32 if f32 else lib.twb_twed_batch_f64
-    _lib.check(fn(_ptr(va), oa.ctypes.data_as(_pi64), nA, _ptr(ta), _ptr(vb),
-                  None if ob is None else ob.ctypes.data_as(_pi64), nB, _ptr(tb), dim,
-                  params.nu, params.lam, params.degree, int(bool(symmetric)), int(row_begin),
-                  int(row_end), int(device), _ptr(out)))
+
+    def solve(r0, r1, dev, dst):
+        _lib.check(fn(_ptr(va), oa.ctypes.data_as(_pi64), nA, _ptr(ta), _ptr(vb),
+                      None if ob is None else ob.ctypes.data_as(_pi64), nB, _ptr(tb), dim,
+                      params.nu, params.lam, params.degree, int(bool(symmetric)), int(r0),
+                      int(r1), int(dev), _ptr(dst)))
+
+    if not isinstance(device, (list, tuple, np.ndarray)):
+        solve(row_begin, row_end, device, out)
+        return out
+    # Several devices in this process: contiguous row blocks balanced by work
+    # (pairs j >= i for the triangle; the lengths of ragged rows), one host
+    # thread per device (ctypes releases the GIL), no collective: every block
+    # lands in its rows of `out`; the triangle's mirror is written after.
+    from .distributed import row_bounds
+    devs = [int(d) for d in device]
+    if not devs:
+        raise ValueError("device list must be non-empty")
+    lens = np.diff(oa)[row_begin:row_end].astype(np.float64)
+    if symmetric:
+        lens = lens * np.arange(nB - row_begin, nB - row_end, -1, dtype=np.float64)
+    bounds = row_bounds(row_end - row_begin, len(devs), False, weights=lens)
+    errors = []
+
+    def run(k):
+        lo, hi = bounds[k]
+        if hi > lo:
+            try:
+                solve(row_begin + lo, row_begin + hi, devs[k], out[lo:hi])
+            except Exception as exc:  # re-raised on the calling thread
+                errors.append(exc)
+
+    threads = [threading.Thread(target=run, args=(k,)) for k in range(len(devs))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    if symmetric and row_begin == 0 and row_end == nA:
+        _mirror_upper_blocked(out)
     return out
+
+
+def _mirror_upper_blocked(m: np.ndarray, block: int = 1024) -> None:
+    """m[j, i] = m[i, j] for j > i, in row blocks (no n x n temporaries)."""
+    n = m.shape[0]
+    for i0 in range(0, n, block):
+        i1 = min(n, i0 + block)
+        if i0 > 0:
+            m[i0:i1, :i0] = m[:i0, i0:i1].T
+        d = m[i0:i1, i0:i1]
+        il = np.tril_indices(i1 - i0, -1)
+        d[il] = d.T[il]
 
 
 def twed_batch(AA, TAA=None, BB=None, TBB=None, nu=1.0, lamb=None, degree=2, tri=None, *,

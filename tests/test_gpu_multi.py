@@ -70,3 +70,31 @@ def test_ring_bad_device_raises(twb):
     a = np.arange(100.0)
     with pytest.raises(ValueError, match="out of range"):
         twb.twed(a, a, a, a, 1.0, 1.0, 2, device=[0, 99])
+
+
+@pytest.mark.parametrize("na,nb", [(1, 1), (1, 7), (5, 3), (40, 1000), (1000, 40), (3000, 2999)])
+def test_ring_tiny_and_skewed_shapes(twb, na, nb):
+    """Fewer stripes than kernels (parts left without a CTA drop out of the ring)."""
+    rng = np.random.default_rng(na * 1000 + nb)
+    a = np.cumsum(rng.standard_normal((na, 2)), axis=0)
+    b = np.cumsum(rng.standard_normal((nb, 2)), axis=0)
+    ta, tb = np.arange(na, dtype=float), np.arange(nb, dtype=float)
+    one = twb.twed(a, ta, b, tb, 1.0, 1.0, 2)
+    assert twb.twed(a, ta, b, tb, 1.0, 1.0, 2, device=[0, 0, 0]) == one
+
+
+@pytest.mark.parametrize("tri", [False, True])
+def test_batch_over_device_list(twb, tri):
+    """twed_batch(..., device=[...]): row blocks on several devices (here the one
+    B200 twice), one host thread each; identical to the single-device matrix."""
+    rng = np.random.default_rng(7)
+    series = [np.cumsum(rng.standard_normal((int(n), 2)), axis=0)
+              for n in rng.integers(5, 300, 57)]
+    one = twb.twed_batch(series, None, None, None, 1.0, 1.0, 2, tri)
+    two = twb.twed_batch(series, None, None, None, 1.0, 1.0, 2, tri, device=[0, 0, 0])
+    assert np.array_equal(one, two)
+    if not tri:
+        other = [np.cumsum(rng.standard_normal((64, 2)), axis=0) for _ in range(9)]
+        one = twb.twed_batch(series, None, other, None, 1.0, 1.0, 2)
+        two = twb.twed_batch(series, None, other, None, 1.0, 1.0, 2, device=[0, 0])
+        assert np.array_equal(one, two)

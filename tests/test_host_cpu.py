@@ -100,3 +100,17 @@ def test_symbols_documented_in_integration():
     text = (REPO / "INTEGRATION.md").read_text()
     for s in ("twb_twed_f64", "twb_twed_batch_f64", "twb_band_solve_f64"):
         assert s in text
+
+
+def test_blocked_mirror_matches_reference_mirror():
+    """The in-process multi-device batch mirrors the triangle in row blocks
+    (engine.py:223-225: out[j, i] = out[i, j] for i < j)."""
+    from paper_2007_16135_b200.api import _mirror_upper_blocked
+    from paper_2007_16135_b200.distributed import mirror_upper_numpy
+    rng = np.random.default_rng(0)
+    for n in (1, 2, 255, 256, 257, 1000):
+        m = rng.standard_normal((n, n))
+        a, b = m.copy(), m.copy()
+        _mirror_upper_blocked(a, block=256)
+        mirror_upper_numpy(b)
+        assert np.array_equal(a, b), n
