@@ -538,6 +538,29 @@ def run_pair_all_gpus(args, world, rank, host):
     return res
 
 
+def batch_reference_rate(S, TS, n, d, count=240):
+    """The reference's twed_batch (engine.py:183-226: per-pair serial band solves
+    on a thread pool, all host cores) on a bounded sample of config 5: the
+    symmetric batch of the first `count` series (fp32-rounded inputs, fp64)."""
+    tb = load_reference()
+    if tb is None:
+        return None
+    threads = os.cpu_count() or 1
+    series = [tb.TimeSeries(S[k * n:(k + 1) * n].astype(np.float64),
+                            TS[k * n:(k + 1) * n].astype(np.float64)) for k in range(count)]
+    params = tb.TwedParams(1.0, 1.0, 2)
+    w8 = series[:8]
+    warm = tb.BatchSpec(w8, w8, params, symmetric=True, workers=threads)
+    tb.twed_batch(warm)
+    t0 = time.perf_counter()
+    tb.twed_batch(tb.BatchSpec(series, series, params, symmetric=True, workers=threads))
+    dt = time.perf_counter() - t0
+    pairs = count * (count + 1) // 2
+    return {"value": pairs / dt, "unit": "pairs/s", "cores": threads, "seconds": dt,
+            "sample": f"symmetric batch of the first {count} config-5 series ({pairs} pairs)",
+            "what": "twedband.twed_batch (the reference package, thread pool of serial band solves)"}
+
+
 def run_batch_cfg5(args, world, rank, local):
     import torch
 
@@ -594,7 +617,11 @@ def run_batch_cfg5(args, world, rank, local):
     cells = pairs * float(n) * n
     peak = lib.twb_probe_add_rate(0, local)
     kms = max_over_ranks(float(np.mean(ks)), world)
-    return {"metric": "twed_batch pairs/s (tri 10k x 10k, n=128, d=2, fp32)",
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = batch_reference_rate(S, TS, n, d)
+    return {"cpu_reference": cpu,
+            "metric": "twed_batch pairs/s (tri 10k x 10k, n=128, d=2, fp32)",
             "workload": "cfg5", "pairs": pairs, "value": pairs / (ms * 1e-3), "unit": "pairs/s",
             "gcups": cells / (ms * 1e-3) / 1e9, "ms_per_step": ms, "n_gpus": world,
             "scaling": "strong",
