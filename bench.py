@@ -97,10 +97,18 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
+    def mark_start(self):
+        self.i0 = len(self.lines)
+
+    def mark_end(self):
+        time.sleep(0.25)  # the sample in flight at the end of the region
+        self.i1 = len(self.lines)
+
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
+        lines = self.lines[getattr(self, "i0", 0):getattr(self, "i1", len(self.lines))]
+        for line in lines:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 9:
                 continue
@@ -315,7 +323,11 @@ def run_ours(args, world, rank, local):
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    # nvidia-smi starts (and settles) before the timed region: its start-up
+    # can stall the GPU; only the samples taken during the region are kept
     with ClockSampler(local) as clocks:
+        time.sleep(1.0)
+        clocks.mark_start()
         ev0.record(stream)
         for _ in range(args.steps):
             flush_l2(l2_flush)
@@ -323,6 +335,7 @@ def run_ours(args, world, rank, local):
             kernel_ms.append(lib.twb_last_kernel_ms())
         ev1.record(stream)
         torch.cuda.synchronize()
+        clocks.mark_end()
     barrier(world)
     launches = _lib.take_launch_count()  # libtwb200 kernels only (the L2 flush is torch's)
     elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1), world)
