@@ -98,3 +98,15 @@ def test_batch_over_device_list(twb, tri):
         one = twb.twed_batch(series, None, other, None, 1.0, 1.0, 2)
         two = twb.twed_batch(series, None, other, None, 1.0, 1.0, 2, device=[0, 0])
         assert np.array_equal(one, two)
+
+
+@pytest.mark.parametrize("degree,d", [(1, 3), (3, 2), (2, 1), (2, 4)])
+def test_ring_other_degrees_and_dims(twb, degree, d):
+    """Degree 1 (sums of |diff|), degree 3 (the NaN-exact compare chain with a
+    runtime degree), d = 1 and d = 4 through the multi-kernel ring."""
+    rng = np.random.default_rng(degree * 10 + d)
+    a = np.cumsum(rng.standard_normal((12_000, d)), axis=0)
+    b = np.cumsum(rng.standard_normal((9_000, d)), axis=0)
+    ta, tb = np.arange(len(a), dtype=float), np.arange(len(b), dtype=float)
+    one = twb.twed(a, ta, b, tb, 0.5, 0.25, degree)
+    assert twb.twed(a, ta, b, tb, 0.5, 0.25, degree, device=[0, 0]) == one
