@@ -23,7 +23,7 @@ from .api import (
 from .core import InvalidInputError, TimeSeries, TwedParams
 from ._lib import TwbError, device_count
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"
 
 __all__ = [
     "InvalidInputError",

@@ -919,7 +919,7 @@ double twb_probe_add_rate(int fp64, int device) {
     return ops / (best * 1e-3);
 }
 
-int twb_version(void) { return 100; }
+int twb_version(void) { return 200; }
 
 size_t twb_last_error(char* buf, size_t len) {
     if (buf && len) {

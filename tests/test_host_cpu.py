@@ -27,7 +27,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(_lib.exported_symbols())
-    assert lib.twb_version() == 100
+    assert lib.twb_version() == 200
     assert isinstance(ctypes.CDLL(str(_lib.LIB_PATH)), ctypes.CDLL)
 
 
