@@ -362,6 +362,15 @@ def run_ours(args, world, rank, local):
            "ms_per_step": e2e_s / args.steps * 1e3, "api": "paper_2007_16135_b200.twed"}
 
     # ---- roofline -----------------------------------------------------------
+    import ctypes
+    shape = [ctypes.c_int64(0) for _ in range(3)]
+    lib.twb_last_wave_shape(*(ctypes.byref(x) for x in shape))
+    stripes, rows_per_stripe, ctas = (int(x.value) for x in shape)
+    # bytes a launch must move: the two series (values + times) once, and each
+    # stripe's bottom row (z and d, 16 B per column) written and read back once
+    # (z is fp64 in every pair mode; d is fp32 in the fp32 mode)
+    boundary = 2 * stripes * (n + 1) * (8 + (4 if f32 else 8))
+    alg_bytes = sum(x.nbytes for x in host) + boundary
     peak_ops = lib.twb_probe_add_rate(0 if f32 else 1, local)
     achieved_ops = FLOPS_PER_CELL[d] * cells / (kmean * 1e-3)
     traffic = None
@@ -382,7 +391,12 @@ def run_ours(args, world, rank, local):
         "peak_source": ("twb_probe_add_rate: measured independent-add throughput of the "
                         f"{'FP32' if f32 else 'FP64'} pipe on this GPU, 1 op per lane per add "
                         "(MEASURED_PEAKS.json has no FP64/FP32-ALU peak)"),
-        "algorithmic_bytes_per_cell": 0.0,
+        "algorithmic_bytes_per_launch": alg_bytes,
+        "algorithmic_bytes_per_cell": alg_bytes / cells,
+        "sweep_shape": {"stripes": stripes, "rows_per_stripe": rows_per_stripe, "ctas": ctas},
+        "traffic_note": ("ncu DRAM bytes of one cfg3 launch (profiles/ncu_summary.json): the "
+                         "stripes' bottom rows written back from L2; the next stripe reads "
+                         "them from L2"),
     }
 
     # ---- batch (config 5: tri 10k x 10k, n=128, d=2, fp32), sharded over ranks -------

@@ -35,6 +35,7 @@ _SIGS = {
     "twb_take_launch_count": (_i64, []),
     "twb_set_kernel_timing": (None, [ctypes.c_int]),
     "twb_last_kernel_ms": (ctypes.c_float, []),
+    "twb_last_wave_shape": (None, [_pi64, _pi64, _pi64]),
     "twb_probe_add_rate": (ctypes.c_double, [ctypes.c_int, ctypes.c_int]),
     "twb_selftest_sqrt": (_i64, [_i64, ctypes.c_uint64, _i32, ctypes.POINTER(_i64)]),
     "twb_twed_f64": (ctypes.c_int, [_pd, _i64, _pd, _pd, _i64, _pd, _i32, _d, _d, _i32, _i32, _pd]),

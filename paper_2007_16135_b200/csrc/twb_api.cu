@@ -948,6 +948,12 @@ int64_t twb_take_launch_count(void) {
 
 void twb_set_kernel_timing(int enable) { t_timing = enable != 0; }
 
+void twb_last_wave_shape(int64_t* stripes, int64_t* rows_per_stripe, int64_t* ctas) {
+    if (stripes) *stripes = t_ctx.wave_stripes;
+    if (rows_per_stripe) *rows_per_stripe = t_ctx.wave_rows;
+    if (ctas) *ctas = t_ctx.wave_ctas;
+}
+
 float twb_last_kernel_ms(void) {
     if (!t_timing || !t_ctx.ev1) return -1.f;
     if (cudaEventSynchronize(t_ctx.ev1) != cudaSuccess) return -1.f;

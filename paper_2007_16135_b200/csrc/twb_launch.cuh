@@ -26,6 +26,7 @@ struct WaveCfg {
 struct LaunchCtx {
     int64_t launches = 0;
     bool timing = false;
+    int64_t wave_stripes = 0, wave_rows = 0, wave_ctas = 0;  // shape of the last sweep
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     void before(cudaStream_t st) {
         if (timing) cudaEventRecord(ev0, st);
@@ -247,6 +248,11 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
         args[l].next_z = nx.gbuf;
         args[l].next_m = nx.gmbuf;
         args[l].next_prog = nx.gprog;
+    }
+    if (pr.gate == nullptr || pr.gate_want == 0) {  // the main sweep (not the gated NaN-exact one)
+        ctx->wave_stripes = S;
+        ctx->wave_rows = H;
+        ctx->wave_ctas = G;
     }
     // TWB_DBG_TIMES=<file>: per-stripe timestamps (single kernel; diagnostics, synchronises)
     const char* dbg_path = nl == 1 && !pr.ring ? getenv("TWB_DBG_TIMES") : nullptr;
