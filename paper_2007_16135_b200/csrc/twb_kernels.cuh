@@ -13,7 +13,10 @@
 //                     CTAs through flag-synchronised global boundary rows
 //                     (st.release.gpu / ld.acquire.gpu progress counters), so
 //                     the anti-diagonal wavefront sweeps without a launch or a
-//                     grid barrier per diagonal.
+//                     grid barrier per diagonal. The ring of CTAs may span
+//                     several kernels (one per device: system-scope links to
+//                     the next kernel's inbox in peer memory).
+//   (lcs_kernel, the bit-parallel LCS sweep, lives in twb_lcs.cu.)
 #pragma once
 
 #include "twb_stripe.cuh"
@@ -655,8 +658,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             zbot[c] = INF;
             mbot[c] = R(0);
         }
-        // Generic step (pipeline fill / drain, NaN-exact mode): lanes' columns
-        // outside [0, ncols) idle.
+        // Generic step (NaN-exact mode, and the fill / drain of rows too short
+        // for the pipelined body): lanes' columns outside [0, ncols) idle.
         auto generic = [&](int st) {
             preamble(st);
             Z zin[C];
