@@ -655,20 +655,52 @@ int twed_batch_dev_impl(const T* dAA, const int64_t* a_off, int64_t nAA, const T
         a.counter = d_counter;
         CK(call_batch<R, Z>(dim, v.P, v.E, v.N1, a, max_rows, st));
     }
-    // Long row-side series: one wavefront solve per pair.
+    // Long row-side series: one wavefront solve per pair. A pair of a few
+    // thousand samples fills only a CTA or two, so the pairs are spread over a
+    // pool of streams and their (cooperative, small-grid) sweeps run side by
+    // side; the pool joins back into the caller's stream.
     if (!long_rows.empty()) {
-        using ZW = double;  // pairs accumulate in fp64 in both precision modes
-        ZW* wout = nullptr;
-        Z* tmp = nullptr;
-        for (int64_t li : long_rows) {
-            const int64_t i = row_begin + li;
-            const int64_t jfirst = tri ? i : 0;
-            for (int64_t j = jfirst; j < nBB; ++j) {
-                Scratch pair_sc(st);
-                // the wave kernel needs Z = double; in fp32-accumulator builds
-                // (R=float, Z=float) rows this long cannot happen: Z=float is
-                // only selected when every series is short.
-                if constexpr (std::is_same<Z, double>::value) {
+        if constexpr (!std::is_same<Z, double>::value) {
+            // the wave kernel needs Z = double; Z = float is only selected when
+            // every series is short
+            return fail(TWB_EUNSUP, "internal: fp32 accumulator with long series");
+        } else {
+            int64_t npairs = 0;
+            for (int64_t li : long_rows) npairs += nBB - (tri ? row_begin + li : 0);
+            const int ns = (int)std::min<int64_t>(32, std::max<int64_t>(npairs, 1));
+            std::vector<cudaStream_t> pool(ns, nullptr);
+            cudaEvent_t fork = nullptr;
+            auto release = [&]() {
+                for (int k = 0; k < ns; ++k) {
+                    if (!pool[k]) continue;
+                    cudaEvent_t joined;
+                    if (cudaEventCreateWithFlags(&joined, cudaEventDisableTiming) == cudaSuccess) {
+                        cudaEventRecord(joined, pool[k]);
+                        cudaStreamWaitEvent(st, joined, 0);
+                        cudaEventDestroy(joined);
+                    }
+                    cudaStreamSynchronize(pool[k]);
+                    cudaStreamDestroy(pool[k]);
+                }
+                if (fork) cudaEventDestroy(fork);
+            };
+            struct PoolGuard {
+                std::function<void()> f;
+                ~PoolGuard() { f(); }
+            } pool_guard{release};
+            CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+            CK(cudaEventRecord(fork, st));  // inputs prepared, zout allocated
+            for (int k = 0; k < ns; ++k) {
+                CK(cudaStreamCreateWithFlags(&pool[k], cudaStreamNonBlocking));
+                CK(cudaStreamWaitEvent(pool[k], fork, 0));
+            }
+            int64_t q = 0;
+            for (int64_t li : long_rows) {
+                const int64_t i = row_begin + li;
+                const int64_t jfirst = tri ? i : 0;
+                for (int64_t j = jfirst; j < nBB; ++j, ++q) {
+                    const int k = (int)(q % ns);
+                    Scratch pair_sc(pool[k]);  // freed stream-ordered after the pair
                     WaveProblem<R, double> pr;
                     pr.A = {VA + a_poff[i] * dim, TmA + a_poff[i], DelA + a_poff[i]};
                     pr.B = {VB + b_poff[j] * dim, TmB + b_poff[j], DelB + b_poff[j]};
@@ -677,15 +709,11 @@ int twed_batch_dev_impl(const T* dAA, const int64_t* a_off, int64_t nAA, const T
                     pr.nu = nu;
                     pr.p = degree;
                     pr.out = zout + li * nBB + j;
-                    CK(call_wave<R, double>(dim, v.P, v.E, v.N1, pr, pair_sc, st));
+                    CK(call_wave<R, double>(dim, v.P, v.E, v.N1, pr, pair_sc, pool[k]));
                     if (pair_sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
                     if (mirror && j != i)
                         CK(cudaMemcpyAsync(zout + j * nBB + i, zout + li * nBB + j, sizeof(double),
-                                           cudaMemcpyDeviceToDevice, st));
-                } else {
-                    (void)wout;
-                    (void)tmp;
-                    return fail(TWB_EUNSUP, "internal: fp32 accumulator with long series");
+                                           cudaMemcpyDeviceToDevice, pool[k]));
                 }
             }
         }

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdio>
 #include <vector>
 
@@ -134,18 +135,28 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
     // SM slots per part (parts sharing a device split it)
     std::vector<int64_t> capp(np);
     int64_t cap = 0;
+    // SM slots of this kernel per device, queried once per device (the batch
+    // path launches one sweep per long pair: the attribute call and the
+    // occupancy query would otherwise dominate its host time)
+    static std::atomic<int> slots_cache[64];
     for (int q = 0; q < np; ++q) {
-        int sms = 0, occ = 0, share = 0;
+        int share = 0;
         for (int r = 0; r < np; ++r) share += parts[r].device == parts[q].device;
-        cudaError_t e = cudaSetDevice(parts[q].device);
-        if (e == cudaSuccess)
-            e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, parts[q].device);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * 32, smem);
-        if (e != cudaSuccess) return e;
-        if (occ < 1) return cudaErrorLaunchOutOfResources;
-        capp[q] = (int64_t)sms * occ / share;
+        const int dv = parts[q].device;
+        int slots = dv >= 0 && dv < 64 ? slots_cache[dv].load(std::memory_order_relaxed) : 0;
+        if (slots <= 0) {
+            int sms = 0, occ = 0;
+            cudaError_t e = cudaSetDevice(dv);
+            if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dv);
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, W * 32, smem);
+            if (e != cudaSuccess) return e;
+            if (occ < 1) return cudaErrorLaunchOutOfResources;
+            slots = sms * occ;
+            if (dv >= 0 && dv < 64) slots_cache[dv].store(slots, std::memory_order_relaxed);
+        }
+        capp[q] = (int64_t)slots / share;
         cap += capp[q];
     }
     cudaSetDevice(cur_dev);

@@ -110,3 +110,19 @@ def test_ring_other_degrees_and_dims(twb, degree, d):
     ta, tb = np.arange(len(a), dtype=float), np.arange(len(b), dtype=float)
     one = twb.twed(a, ta, b, tb, 0.5, 0.25, degree)
     assert twb.twed(a, ta, b, tb, 0.5, 0.25, degree, device=[0, 0]) == one
+
+
+@pytest.mark.parametrize("tri", [False, True])
+def test_batch_long_rows_on_stream_pool(twb, tri):
+    """Row-side series longer than the warp kernel's 256 samples go through
+    per-pair wavefront sweeps spread over a pool of streams: entries equal the
+    single-pair results, the triangle layout included."""
+    rng = np.random.default_rng(11)
+    lens = [200, 257, 300, 511, 900, 64, 1500, 256, 700, 333, 40]
+    series = [np.cumsum(rng.standard_normal((n, 2)), axis=0) for n in lens]
+    R = twb.twed_batch(series, None, None, None, 1.0, 1.0, 2, tri)
+    for i in range(len(series)):
+        for j in range(len(series)):
+            want = twb.twed(series[i], np.arange(lens[i], dtype=float), series[j],
+                            np.arange(lens[j], dtype=float), 1.0, 1.0, 2)
+            assert R[i, j] == want, (i, j)
