@@ -310,26 +310,34 @@ def run_ours(args, world, rank, local):
         twb.twed_dev(*dev_in, nu=1.0, lamb=1.0, degree=2, out=out, stream=stream)
 
     lib.twb_set_kernel_timing(1)
-    for _ in range(args.warmup):
-        step()
-        lib.twb_last_kernel_ms()
-    torch.cuda.synchronize()
-    result = out.item()
-
-    # ---- device-resident timed region -------------------------------------
-    _lib.take_launch_count()
-    kernel_ms = []
-    barrier(world)
-    torch.cuda.synchronize()
+    # nvidia-smi starts (and settles) before the warm-up; only the samples
+    # taken during the timed region are kept. The warm-up steps are the timed
+    # step exactly (L2 flush included: its kernel is loaded lazily on first
+    # use, which cost the first timed step up to 200 ms when it was not), and
+    # the timed region follows them without an idle gap.
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    # nvidia-smi starts (and settles) before the timed region: its start-up
-    # can stall the GPU; only the samples taken during the region are kept
+    kernel_ms = []
     with ClockSampler(local) as clocks:
         time.sleep(1.0)
+        for _ in range(args.warmup):
+            flush_l2(l2_flush)
+            step()
+            lib.twb_last_kernel_ms()
+        torch.cuda.synchronize()
+        result = out.item()
+
+        # ---- device-resident timed region ---------------------------------
+        _lib.take_launch_count()
+        barrier(world)
+        torch.cuda.synchronize()
         clocks.mark_start()
         ev0.record(stream)
+        step_ev = []
         for _ in range(args.steps):
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            step_ev.append(e)
             flush_l2(l2_flush)
             step()
             kernel_ms.append(lib.twb_last_kernel_ms())
@@ -338,6 +346,9 @@ def run_ours(args, world, rank, local):
         clocks.mark_end()
     barrier(world)
     launches = _lib.take_launch_count()  # libtwb200 kernels only (the L2 flush is torch's)
+    marks = step_ev + [ev1]
+    log("timed steps (ms, event-to-event / kernel):",
+        [(round(a.elapsed_time(b), 2), round(k, 2)) for a, b, k in zip(marks, marks[1:], kernel_ms)])
     elapsed_ms = max_over_ranks(ev0.elapsed_time(ev1), world)
     value = world * args.steps * cells / (elapsed_ms * 1e-3) / 1e9
     ms_per_step = elapsed_ms / args.steps
