@@ -74,6 +74,8 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
+        if os.environ.get("TWB_BENCH_NO_CLOCKS"):  # diagnostics: no sampler at all
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
