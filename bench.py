@@ -30,6 +30,7 @@ is reported in the "batch" object, sharded over the N GPUs (strong scaling).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -331,6 +332,10 @@ def run_ours(args, world, rank, local):
 
         # ---- device-resident timed region ---------------------------------
         _lib.take_launch_count()
+        # no cyclic-GC pass inside the region: a full collection of this
+        # process's objects takes ~100 ms of host time between launches
+        gc.collect()
+        gc.disable()
         barrier(world)
         torch.cuda.synchronize()
         clocks.mark_start()
@@ -346,6 +351,7 @@ def run_ours(args, world, rank, local):
         ev1.record(stream)
         torch.cuda.synchronize()
         clocks.mark_end()
+        gc.enable()
     barrier(world)
     launches = _lib.take_launch_count()  # libtwb200 kernels only (the L2 flush is torch's)
     marks = step_ev + [ev1]
