@@ -435,8 +435,8 @@ def run_ours(args, world, rank, local):
         from oracle import oracle as orc
         threads = os.cpu_count() or 1
         kind = reference_kind()
-        gc, ns, dts = cpu_reference_rate(kind, d, wl["seed"], args.cpu_budget_s, threads)
-        cpu = {"value": gc, "unit": "GCUPS", "cores": threads, "kind": kind,
+        ref_gcups, ns, dts = cpu_reference_rate(kind, d, wl["seed"], args.cpu_budget_s, threads)
+        cpu = {"value": ref_gcups, "unit": "GCUPS", "cores": threads, "kind": kind,
                "sample": reference_sample_text(kind, ns, d, wl["seed"], threads, args.workload)
                + f" ({dts:.1f} s)",
                "host": orc.host_description()}
