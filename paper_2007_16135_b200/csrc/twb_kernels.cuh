@@ -342,9 +342,11 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
 // Wavefront: one long pair.
 // ---------------------------------------------------------------------------
 // A waiting warp backs off so that it does not take issue slots from the warps
-// it shares a sub-partition with (which include the one it waits for).
+// it shares a sub-partition with (which include the one it waits for). B200,
+// n = 1M: d = 1 1008 vs 988 GCUPS with 128 ns, d = 3 486 vs 485; 300k d = 3
+// 385 vs 382 (profiles/r01g_session_ab.log).
 #ifndef TWB_SPIN_NS
-#define TWB_SPIN_NS 0
+#define TWB_SPIN_NS 128
 #endif
 __device__ __forceinline__ void spin_pause() {
     if constexpr (TWB_SPIN_NS > 0) __nanosleep(TWB_SPIN_NS);
