@@ -291,61 +291,131 @@ def prepare_series(series: TimeSeries, params: TwedParams, device=0):
 # Device-resident variants (torch CUDA tensors in, torch CUDA tensor out),
 # the paper's twed_dev: no host copies, caller's stream.
 # ---------------------------------------------------------------------------
+def _check_cuda(name, t, dtype, device, numel=None):
+    """Device-resident arguments: a contiguous CUDA tensor of the given dtype
+    on the given device (and size). A mismatch would otherwise read or write
+    out of bounds on the device."""
+    import torch
+
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor, got {type(t).__name__}")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device} (all tensors on one device)")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} has dtype {t.dtype}, expected {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name} has {t.numel()} elements, expected {numel}")
+
+
 def twed_dev(A, TA, B, TB, nu=1.0, lamb=None, degree=2, *, lam=None, out=None, stream=None):
-    """A, TA, B, TB: contiguous CUDA tensors (float64 or float32). Returns a 1-element
-    float64 CUDA tensor (or fills ``out``). Validation of timestamps is the caller's
-    responsibility (no host round trip)."""
+    """A, TA, B, TB: contiguous CUDA tensors (float64 or float32) on one device. Returns
+    a 1-element float64 CUDA tensor (or fills ``out``). Validation of timestamps is the
+    caller's responsibility (no host round trip); shapes, dtypes and devices are checked."""
     import torch
 
     params = TwedParams(nu=nu, lam=_lam(lamb, lam), degree=degree)
     lib = _lib.load()
+    if not isinstance(A, torch.Tensor) or not isinstance(B, torch.Tensor):
+        raise TypeError("twed_dev takes torch CUDA tensors")
+    if A.dim() not in (1, 2) or B.dim() not in (1, 2):
+        raise ValueError("values must be 1-D or 2-D (n samples by d components)")
     A2 = A if A.dim() == 2 else A.reshape(-1, 1)
     B2 = B if B.dim() == 2 else B.reshape(-1, 1)
     if A2.shape[1] != B2.shape[1]:
         raise ValueError(f"series dimensions differ: A has d={A2.shape[1]}, B has d={B2.shape[1]}")
-    for t in (A2, TA, B2, TB):
-        if not t.is_cuda or not t.is_contiguous():
-            raise ValueError("twed_dev needs contiguous CUDA tensors")
+    if A2.dtype not in (torch.float64, torch.float32):
+        raise ValueError(f"values must be float64 or float32, got {A2.dtype}")
+    dev = A2.device
+    _check_cuda("A", A2, A2.dtype, dev)
+    _check_cuda("B", B2, A2.dtype, dev)
+    _check_cuda("TA", TA, A2.dtype, dev, A2.shape[0])
+    _check_cuda("TB", TB, A2.dtype, dev, B2.shape[0])
+    if A2.shape[0] < 1 or B2.shape[0] < 1:
+        raise InvalidInputError("a time series needs at least one sample")
     if out is None:
-        out = torch.empty(1, dtype=torch.float64, device=A.device)
-    st = stream if stream is not None else torch.cuda.current_stream(A.device)
+        out = torch.empty(1, dtype=torch.float64, device=dev)
+    _check_cuda("out", out, torch.float64, dev)
+    if out.numel() < 1:
+        raise ValueError("out needs one element")
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
     fn = lib.twb_twed_dev_f64 if A2.dtype == torch.float64 else lib.twb_twed_dev_f32
-    with torch.cuda.device(A.device):
+    with torch.cuda.device(dev):
         _lib.check(fn(A2.data_ptr(), A2.shape[0], TA.data_ptr(), B2.data_ptr(), B2.shape[0],
                       TB.data_ptr(), A2.shape[1], params.nu, params.lam, params.degree,
                       st.cuda_stream, out.data_ptr()))
     return out
 
 
+def _check_offsets(name, off, rows):
+    off = np.ascontiguousarray(off, dtype=np.int64)
+    if off.ndim != 1 or off.shape[0] < 2:
+        raise InvalidInputError("batch lists must be nonempty")
+    if off[0] != 0:
+        raise ValueError(f"{name}[0] must be 0, got {off[0]}")
+    if np.any(np.diff(off) < 1):
+        raise InvalidInputError("a time series needs at least one sample")
+    if off[-1] != rows:
+        raise ValueError(f"{name}[-1] = {off[-1]} does not match the {rows} packed samples")
+    return off
+
+
 def twed_batch_dev(AA, a_off, TAA, BB=None, b_off=None, TBB=None, nu=1.0, lamb=None, degree=2,
                    tri=False, *, lam=None, row_begin=0, row_end=None, out=None, stream=None):
-    """Packed device inputs: AA (N_total, d) CUDA tensor, a_off host int64 offsets
-    (N+1,), TAA (N_total,). Returns the (row_end-row_begin, nB) block on the device."""
+    """Packed device inputs: AA (N_total, d) CUDA tensor, a_off host int64 CSR offsets
+    (N+1,) starting at 0, TAA (N_total,). Returns the (row_end-row_begin, nB) block on the
+    device (AA's dtype). Every tensor is checked (device, dtype, contiguity, size)."""
     import torch
 
     params = TwedParams(nu=nu, lam=_lam(lamb, lam), degree=degree)
     lib = _lib.load()
-    a_off = np.ascontiguousarray(a_off, dtype=np.int64)
+    if not isinstance(AA, torch.Tensor):
+        raise TypeError("twed_batch_dev takes torch CUDA tensors")
+    if AA.dim() not in (1, 2):
+        raise ValueError("packed values must be 1-D or 2-D (samples by components)")
+    AA2 = AA if AA.dim() == 2 else AA.reshape(-1, 1)
+    if AA2.dtype not in (torch.float64, torch.float32):
+        raise ValueError(f"values must be float64 or float32, got {AA2.dtype}")
+    dev, dt = AA2.device, AA2.dtype
+    dim = AA2.shape[1]
+    _check_cuda("AA", AA2, dt, dev)
+    a_off = _check_offsets("a_off", a_off, AA2.shape[0])
+    _check_cuda("TAA", TAA, dt, dev, AA2.shape[0])
     nA = a_off.shape[0] - 1
+    if (BB is None) != (TBB is None) or (BB is None) != (b_off is None):
+        raise ValueError("pass BB, b_off and TBB together (or none of them for a self batch)")
+    BB2 = None
     if BB is not None:
-        b_off = np.ascontiguousarray(b_off, dtype=np.int64)
+        if not isinstance(BB, torch.Tensor) or BB.dim() not in (1, 2):
+            raise ValueError("BB must be a 1-D or 2-D CUDA tensor")
+        BB2 = BB if BB.dim() == 2 else BB.reshape(-1, 1)
+        if BB2.shape[1] != dim:
+            raise InvalidInputError(f"batch series dimensions differ: {BB2.shape[1]} vs {dim}")
+        _check_cuda("BB", BB2, dt, dev)
+        b_off = _check_offsets("b_off", b_off, BB2.shape[0])
+        _check_cuda("TBB", TBB, dt, dev, BB2.shape[0])
         nB = b_off.shape[0] - 1
+        if tri:
+            raise InvalidInputError("symmetric=True requires both lists to be the same collection")
     else:
         nB = nA
     if row_end is None:
         row_end = nA
-    AA2 = AA if AA.dim() == 2 else AA.reshape(-1, 1)
-    dim = AA2.shape[1]
-    f32 = AA2.dtype == torch.float32
+    if not (0 <= row_begin < row_end <= nA):
+        raise ValueError(f"row range [{row_begin}, {row_end}) outside [0, {nA})")
     if out is None:
-        out = torch.empty((row_end - row_begin, nB), dtype=AA2.dtype, device=AA.device)
-    st = stream if stream is not None else torch.cuda.current_stream(AA.device)
-    fn = lib.twb_twed_batch_dev_f32 if f32 else lib.twb_twed_batch_dev_f64
-    with torch.cuda.device(AA.device):
+        out = torch.empty((row_end - row_begin, nB), dtype=dt, device=dev)
+    _check_cuda("out", out, dt, dev, (row_end - row_begin) * nB)
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    fn = lib.twb_twed_batch_dev_f32 if dt == torch.float32 else lib.twb_twed_batch_dev_f64
+    with torch.cuda.device(dev):
         _lib.check(fn(AA2.data_ptr(), a_off.ctypes.data_as(_pi64), nA, TAA.data_ptr(),
-                      None if BB is None else BB.data_ptr(),
-                      None if BB is None else b_off.ctypes.data_as(_pi64), nB,
-                      None if TBB is None else TBB.data_ptr(), dim, params.nu, params.lam,
+                      None if BB2 is None else BB2.data_ptr(),
+                      None if BB2 is None else b_off.ctypes.data_as(_pi64), nB,
+                      None if BB2 is None else TBB.data_ptr(), dim, params.nu, params.lam,
                       params.degree, int(bool(tri)), int(row_begin), int(row_end),
                       st.cuda_stream, out.data_ptr()))
     return out

@@ -105,6 +105,13 @@ def as_series(values, times, label: str, dtype=np.float64) -> TimeSeries:
     return TimeSeries(values, times, dtype)
 
 
+def is_series_like(item) -> bool:
+    """A TimeSeries of the reference package (twedband.TimeSeries, C:22-70):
+    anything with ``values`` and ``timestamps`` arrays."""
+    return (not isinstance(item, (np.ndarray, tuple, list)) and hasattr(item, "values")
+            and hasattr(item, "timestamps"))
+
+
 def as_series_list(items, label: str, dtype=np.float64) -> list[TimeSeries]:
     """warpband._as_series_list (W:56-67): TimeSeries, (values, times) or bare values."""
     out = []
@@ -113,6 +120,8 @@ def as_series_list(items, label: str, dtype=np.float64) -> list[TimeSeries]:
             if item.values.dtype != dtype:
                 item = TimeSeries(item.values, item.timestamps, dtype)
             out.append(item)
+        elif is_series_like(item):  # the reference's own TimeSeries objects
+            out.append(TimeSeries(item.values, item.timestamps, dtype))
         elif isinstance(item, tuple) and len(item) == 2:
             out.append(as_series(item[0], item[1], f"{label}[{k}]", dtype))
         else:

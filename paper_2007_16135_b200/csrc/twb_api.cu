@@ -156,6 +156,26 @@ __global__ void mirror_kernel(T* m, int64_t n) {
     }
 }
 
+// Vt[k * rows + r] = V[r * d + k] (the dim-major copy the runtime-d kernels
+// read columns from), 32x32 tiles through shared memory.
+template <typename R>
+__global__ void transpose_kernel(const R* __restrict__ V, int64_t rows, int d, R* __restrict__ Vt) {
+    __shared__ R tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.x * 32;
+    const int k0 = blockIdx.y * 32;
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int64_t r = r0 + i;
+        const int k = k0 + threadIdx.x;
+        if (r < rows && k < d) tile[i][threadIdx.x] = V[r * d + k];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int k = k0 + i;
+        const int64_t r = r0 + threadIdx.x;
+        if (r < rows && k < d) Vt[k * rows + r] = tile[threadIdx.x][i];
+    }
+}
+
 template <typename T>
 int check_unsafe(const T* d, int64_t n, double limit, int* dflag, cudaStream_t st,
                  double tiny = 0.0) {
@@ -168,15 +188,18 @@ int check_unsafe(const T* d, int64_t n, double limit, int* dflag, cudaStream_t s
 
 // virt: value of the virtual row 0 of V -- 0 (the reference's layout) or
 // +inf (the DP kernels' marker of a virtual column, LaneRows::COL0_BY_INF).
+// Vt (optional): the dim-major copy for the runtime-d kernels, leading
+// dimension ntot + nseries (every prepared row).
 template <typename T, typename R, typename Z>
 int prepare(const T* values, const T* times, const int64_t* d_off, int64_t nseries, int64_t ntot,
             int64_t uniform_n, int dim, double nu, double lam, int degree, R* V, R* Tm, Z* Del,
-            cudaStream_t st, double virt = HUGE_VAL) {
+            cudaStream_t st, double virt = HUGE_VAL, R* Vt = nullptr) {
     const int64_t work = ntot + nseries;
     int blocks = (int)std::min<int64_t>((work + 255) / 256, 148 * 16);
     if (blocks < 1) blocks = 1;
     prepare_kernel<T, R, Z><<<blocks, 256, 0, st>>>(values, times, d_off, nseries, ntot, uniform_n,
-                                                    dim, nu, lam, degree, virt, V, Tm, Del);
+                                                    dim, nu, lam, degree, virt, V, Tm, Del, Vt,
+                                                    work);
     ++t_launches;
     CK(cudaGetLastError());
     return 0;
@@ -195,10 +218,22 @@ LaunchCtx* ctx_begin() {
     return &t_ctx;
 }
 
+// Dimensions 1..4 have compile-time kernels; any other d (and every d with
+// TWB_FORCE_DYN=1, a test hook) runs the runtime-d kernels (D == 0).
+bool use_dyn(int dim) {
+    static const bool force = getenv("TWB_FORCE_DYN") && atoi(getenv("TWB_FORCE_DYN")) != 0;
+    return dim > 4 || force;
+}
+
 template <typename R, typename Z>
 cudaError_t call_wave(int dim, int P, bool E, bool N1, const WaveProblem<R, Z>& pr, Scratch& sc,
                       cudaStream_t st) {
     Alloc al{scratch_alloc, &sc};
+    if (use_dyn(dim)) {
+        WaveProblem<R, Z> p2 = pr;
+        p2.dd = dim;
+        return wave_d<0, R, Z>(P, E, N1, p2, al, st, ctx_begin());
+    }
     switch (dim) {
         case 1: return wave_d<1, R, Z>(P, E, N1, pr, al, st, ctx_begin());
         case 2: return wave_d<2, R, Z>(P, E, N1, pr, al, st, ctx_begin());
@@ -210,12 +245,18 @@ cudaError_t call_wave(int dim, int P, bool E, bool N1, const WaveProblem<R, Z>& 
 
 template <typename R, typename Z>
 cudaError_t call_batch(int dim, int P, bool E, bool N1, const BatchArgs<R, Z>& a, int64_t max_rows,
-                       cudaStream_t st) {
+                       Scratch& sc, cudaStream_t st) {
+    Alloc al{scratch_alloc, &sc};
+    if (use_dyn(dim)) {
+        BatchArgs<R, Z> a2 = a;
+        a2.dd = dim;
+        return batch_d<0, R, Z>(P, E, N1, a2, max_rows, al, st, ctx_begin());
+    }
     switch (dim) {
-        case 1: return batch_d<1, R, Z>(P, E, N1, a, max_rows, st, ctx_begin());
-        case 2: return batch_d<2, R, Z>(P, E, N1, a, max_rows, st, ctx_begin());
-        case 3: return batch_d<3, R, Z>(P, E, N1, a, max_rows, st, ctx_begin());
-        case 4: return batch_d<4, R, Z>(P, E, N1, a, max_rows, st, ctx_begin());
+        case 1: return batch_d<1, R, Z>(P, E, N1, a, max_rows, al, st, ctx_begin());
+        case 2: return batch_d<2, R, Z>(P, E, N1, a, max_rows, al, st, ctx_begin());
+        case 3: return batch_d<3, R, Z>(P, E, N1, a, max_rows, al, st, ctx_begin());
+        case 4: return batch_d<4, R, Z>(P, E, N1, a, max_rows, al, st, ctx_begin());
     }
     return cudaErrorInvalidValue;
 }
@@ -223,8 +264,6 @@ cudaError_t call_batch(int dim, int P, bool E, bool N1, const BatchArgs<R, Z>& a
 int check_params(int64_t nA, int64_t nB, int dim, double nu, double lam, int degree) {
     if (nA < 1 || nB < 1) return fail(TWB_EINVAL, "a time series needs at least one sample");
     if (dim < 1) return fail(TWB_EINVAL, "samples need at least one component");
-    if (dim > 4)
-        return fail(TWB_EUNSUP, "dim=%d: this build compiles kernels for 1 <= dim <= 4", dim);
     if (!(nu >= 0)) return fail(TWB_EINVAL, "nu must be >= 0, got %g", nu);
     if (!(lam >= 0)) return fail(TWB_EINVAL, "lam must be >= 0, got %g", lam);
     if (degree < 1) return fail(TWB_EINVAL, "degree must be a positive integer, got %d", degree);
@@ -245,9 +284,14 @@ Variant pick_variant(int dim, int degree, double nu, double lam, bool unsafe_inp
     return v;
 }
 
+// Values below the limit keep every sum of squared differences finite and,
+// in fp64, inside the branch-free square root's range (<= 2^1004): d terms of
+// (2 * limit)^2 each, so the limit shrinks with d above 4.
 template <typename T>
-constexpr double safe_limit() {
-    return sizeof(T) == 8 ? 0x1p500 : 0x1p60;
+double safe_limit(int dim = 1) {
+    double lim = sizeof(T) == 8 ? 0x1p500 : 0x1p60;
+    for (int d = 4; d < dim; d *= 4) lim *= 0.5;
+    return lim;
 }
 template <typename R>
 constexpr double safe_tiny() {
@@ -266,24 +310,31 @@ int twed_pair_dev(const T* dA, int64_t nA, const T* dTA, const T* dB, int64_t nB
     int* dflag = sc.get_n<int>(1);
     if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
     CK(cudaMemsetAsync(dflag, 0, sizeof(int), st));
-    const double lim = safe_limit<R>();
+    const double lim = safe_limit<R>(dim);
     check_unsafe(dA, nA * dim, lim, dflag, st, safe_tiny<R>());
     check_unsafe(dTA, nA, lim, dflag, st);
     check_unsafe(dB, nB * dim, lim, dflag, st, safe_tiny<R>());
     check_unsafe(dTB, nB, lim, dflag, st);
 
+    const bool dyn = use_dyn(dim);
     R* V[2] = {sc.get_n<R>((nA + 1) * dim), sc.get_n<R>((nB + 1) * dim)};
     R* Tm[2] = {sc.get_n<R>(nA + 1), sc.get_n<R>(nB + 1)};
     Z* Del[2] = {sc.get_n<Z>(nA + 1), sc.get_n<Z>(nB + 1)};
+    R* Vt[2] = {nullptr, nullptr};
+    if (dyn) {
+        Vt[0] = sc.get_n<R>((nA + 1) * dim);
+        Vt[1] = sc.get_n<R>((nB + 1) * dim);
+    }
     Z* zout = sc.get_n<Z>(1);
     if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
     int rc;
     if ((rc = prepare<T, R, Z>(dA, dTA, nullptr, 1, nA, nA, dim, nu, lam, degree, V[0], Tm[0],
-                               Del[0], st)))
+                               Del[0], st, HUGE_VAL, Vt[0])))
         return rc;
     if ((rc = prepare<T, R, Z>(dB, dTB, nullptr, 1, nB, nB, dim, nu, lam, degree, V[1], Tm[1],
-                               Del[1], st)))
+                               Del[1], st, HUGE_VAL, Vt[1])))
         return rc;
+    const int64_t ldt[2] = {nA + 1, nB + 1};
     // No host round trip: the data-dependent choice between the proven-safe
     // sweep and the NaN-exact one is made on the device. Both are launched,
     // gated on the check's flag; the one not wanted returns at once. The call
@@ -301,8 +352,8 @@ int twed_pair_dev(const T* dA, int64_t nA, const T* dTA, const T* dB, int64_t nB
             std::swap(na, nb);
         }
         WaveProblem<R, Z> pr;
-        pr.A = {V[ra], Tm[ra], Del[ra]};
-        pr.B = {V[rb], Tm[rb], Del[rb]};
+        pr.A = {V[ra], Tm[ra], Del[ra], Vt[ra], ldt[ra]};
+        pr.B = {V[rb], Tm[rb], Del[rb], Vt[rb], ldt[rb]};
         pr.nA = na;
         pr.nB = nb;
         pr.nu = nu;
@@ -401,6 +452,7 @@ int twed_pair_multi(const T* A, int64_t nA, const T* TA, const T* B, int64_t nB,
         R* V[2];
         R* Tm[2];
         Z* Del[2];
+        R* Vt[2] = {nullptr, nullptr};
         Z* zout;
         int* dflag;
     };
@@ -421,7 +473,9 @@ int twed_pair_multi(const T* A, int64_t nA, const T* TA, const T* B, int64_t nB,
         std::function<void()> f;
         ~Guard() { f(); }
     } guard{cleanup};
-    const double lim = safe_limit<R>();
+    const double lim = safe_limit<R>(dim);
+    const bool dyn = use_dyn(dim);
+    const int64_t ldt[2] = {nA + 1, nB + 1};
     for (int q = 0; q < ndev; ++q) {
         Part& pt = parts[q];
         pt.dev = devices[q];
@@ -441,6 +495,10 @@ int twed_pair_multi(const T* A, int64_t nA, const T* TA, const T* B, int64_t nB,
         pt.Tm[1] = sc.get_n<R>(nB + 1);
         pt.Del[0] = sc.get_n<Z>(nA + 1);
         pt.Del[1] = sc.get_n<Z>(nB + 1);
+        if (dyn) {
+            pt.Vt[0] = sc.get_n<R>((nA + 1) * dim);
+            pt.Vt[1] = sc.get_n<R>((nB + 1) * dim);
+        }
         pt.zout = sc.get_n<Z>(1);
         if (sc.failed) return fail(TWB_ENOMEM, "device allocation failed on device %d", pt.dev);
         CK(cudaMemcpyAsync(dA, A, sizeof(T) * nA * dim, cudaMemcpyHostToDevice, pt.st));
@@ -453,10 +511,10 @@ int twed_pair_multi(const T* A, int64_t nA, const T* TA, const T* B, int64_t nB,
         check_unsafe(dB, nB * dim, lim, pt.dflag, pt.st, safe_tiny<R>());
         check_unsafe(dTB, nB, lim, pt.dflag, pt.st);
         if ((rc = prepare<T, R, Z>(dA, dTA, nullptr, 1, nA, nA, dim, nu, lam, degree, pt.V[0],
-                                   pt.Tm[0], pt.Del[0], pt.st)))
+                                   pt.Tm[0], pt.Del[0], pt.st, HUGE_VAL, pt.Vt[0])))
             return rc;
         if ((rc = prepare<T, R, Z>(dB, dTB, nullptr, 1, nB, nB, dim, nu, lam, degree, pt.V[1],
-                                   pt.Tm[1], pt.Del[1], pt.st)))
+                                   pt.Tm[1], pt.Del[1], pt.st, HUGE_VAL, pt.Vt[1])))
             return rc;
     }
     int hflag = 0;
@@ -477,8 +535,8 @@ int twed_pair_multi(const T* A, int64_t nA, const T* TA, const T* B, int64_t nB,
     for (int q = 0; q < ndev; ++q) {
         Part& pt = parts[q];
         CK(cudaStreamSynchronize(pt.st));  // inputs prepared on every part
-        wp[q] = WavePart<R, Z>{pt.dev, pt.st, {pt.V[ra], pt.Tm[ra], pt.Del[ra]},
-                               {pt.V[rb], pt.Tm[rb], pt.Del[rb]}, pt.zout,
+        wp[q] = WavePart<R, Z>{pt.dev, pt.st, {pt.V[ra], pt.Tm[ra], pt.Del[ra], pt.Vt[ra], ldt[ra]},
+                               {pt.V[rb], pt.Tm[rb], pt.Del[rb], pt.Vt[rb], ldt[rb]}, pt.zout,
                                Alloc{scratch_alloc, pt.sc}};
     }
     long long timeout_ms = 20000;
@@ -561,6 +619,9 @@ int twed_batch_dev_impl(const T* dAA, const int64_t* a_off, int64_t nAA, const T
         TmB = sc.get_n<R>(totB + nBB);
         DelB = sc.get_n<Z>(totB + nBB);
     }
+    // runtime-d kernels read the columns (the B side) dim-major
+    R* VtB = use_dyn(dim) ? sc.get_n<R>((totB + nBB) * dim) : nullptr;
+    const int64_t ldtB = totB + nBB;
     if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
     CK(cudaMemsetAsync(dflag, 0, sizeof(int), st));
     CK(cudaMemcpyAsync(d_aoff, a_off, sizeof(int64_t) * (nAA + 1), cudaMemcpyHostToDevice, st));
@@ -569,7 +630,7 @@ int twed_batch_dev_impl(const T* dAA, const int64_t* a_off, int64_t nAA, const T
         CK(cudaMemcpyAsync(d_boff, b_off, sizeof(int64_t) * (nBB + 1), cudaMemcpyHostToDevice, st));
     }
     CK(cudaMemcpyAsync(d_bpoff, b_poff.data(), sizeof(int64_t) * (nBB + 1), cudaMemcpyHostToDevice, st));
-    const double lim = safe_limit<R>();
+    const double lim = safe_limit<R>(dim);
     check_unsafe(dAA, totA * dim, lim, dflag, st, safe_tiny<R>());
     check_unsafe(dTAA, totA, lim, dflag, st);
     if (!self) {
@@ -580,11 +641,11 @@ int twed_batch_dev_impl(const T* dAA, const int64_t* a_off, int64_t nAA, const T
     CK(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
     int rc;
     if ((rc = prepare<T, R, Z>(dAA, dTAA, d_aoff, nAA, totA, uniform(a_off, nAA), dim, nu, lam,
-                               degree, VA, TmA, DelA, st)))
+                               degree, VA, TmA, DelA, st, HUGE_VAL, self ? VtB : nullptr)))
         return rc;
     if (!self &&
         (rc = prepare<T, R, Z>(dBB, dTBB, d_boff, nBB, totB, uniform(b_off, nBB), dim, nu, lam,
-                               degree, VB, TmB, DelB, st)))
+                               degree, VB, TmB, DelB, st, HUGE_VAL, VtB)))
         return rc;
 
     // Output block: the kernel writes only solved entries (+ mirror).
@@ -636,7 +697,7 @@ int twed_batch_dev_impl(const T* dAA, const int64_t* a_off, int64_t nAA, const T
         CK(cudaMemsetAsync(d_counter, 0, sizeof(unsigned long long), st));
         BatchArgs<R, Z> a;
         a.A = {VA, TmA, DelA};
-        a.B = {VB, TmB, DelB};
+        a.B = {VB, TmB, DelB, VtB, ldtB};
         a.a_poff = d_apoff;
         a.b_poff = d_bpoff;
         a.nBB = nBB;
@@ -653,7 +714,8 @@ int twed_batch_dev_impl(const T* dAA, const int64_t* a_off, int64_t nAA, const T
         a.nu = nu;
         a.p = degree;
         a.counter = d_counter;
-        CK(call_batch<R, Z>(dim, v.P, v.E, v.N1, a, max_rows, st));
+        CK(call_batch<R, Z>(dim, v.P, v.E, v.N1, a, max_rows, sc, st));
+        if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
     }
     // Long row-side series: one wavefront solve per pair. A pair of a few
     // thousand samples fills only a CTA or two, so the pairs are spread over a
@@ -703,7 +765,8 @@ int twed_batch_dev_impl(const T* dAA, const int64_t* a_off, int64_t nAA, const T
                     Scratch pair_sc(pool[k]);  // freed stream-ordered after the pair
                     WaveProblem<R, double> pr;
                     pr.A = {VA + a_poff[i] * dim, TmA + a_poff[i], DelA + a_poff[i]};
-                    pr.B = {VB + b_poff[j] * dim, TmB + b_poff[j], DelB + b_poff[j]};
+                    pr.B = {VB + b_poff[j] * dim, TmB + b_poff[j], DelB + b_poff[j],
+                            VtB ? VtB + b_poff[j] : nullptr, ldtB};
                     pr.nA = a_off[i + 1] - a_off[i];
                     pr.nB = b_off[j + 1] - b_off[j];
                     pr.nu = nu;
@@ -732,6 +795,9 @@ int twed_batch_dev_impl(const T* dAA, const int64_t* a_off, int64_t nAA, const T
 int check_batch(const int64_t* a_off, int64_t nAA, const int64_t* b_off, int64_t nBB, int dim,
                 double nu, double lam, int degree, int64_t row_begin, int64_t row_end) {
     if (!a_off || nAA < 1 || (b_off && nBB < 1)) return fail(TWB_EINVAL, "batch lists must be nonempty");
+    // CSR offsets start at 0 (the packed arrays hold exactly off[n] samples)
+    if (a_off[0] != 0 || (b_off && b_off[0] != 0))
+        return fail(TWB_EINVAL, "CSR offsets must start at 0 (a_off[0] = %lld)", (long long)a_off[0]);
     for (int64_t k = 0; k < nAA; ++k)
         if (a_off[k + 1] - a_off[k] < 1) return fail(TWB_EINVAL, "a time series needs at least one sample");
     if (b_off)
@@ -754,6 +820,8 @@ int twed_batch_dev(const T* dAA, const int64_t* a_off, int64_t nAA, const T* dTA
                          row_end);
     if (rc) return rc;
     if (tri && !self) return fail(TWB_EINVAL, "symmetric=True requires both lists to be the same collection");
+    if (!dAA || !dTAA || !d_out || (!self && (!dTBB || !b_off)))
+        return fail(TWB_EINVAL, "null pointer argument");
     init_pool_current();
     if constexpr (sizeof(T) == 8) {
         return twed_batch_dev_impl<T, double, double, O>(dAA, a_off, nAA, dTAA, dBB, b_off, nBB,
@@ -1007,6 +1075,7 @@ int twb_twed_dev_f64(const double* dA, int64_t nA, const double* dTA, const doub
                      void* stream, double* d_out) {
     int rc = check_params(nA, nB, dim, nu, lam, degree);
     if (rc) return rc;
+    if (!dA || !dTA || !dB || !dTB || !d_out) return fail(TWB_EINVAL, "null pointer argument");
     return twed_pair_dev<double, double, double>(dA, nA, dTA, dB, nB, dTB, dim, nu, lam, degree,
                                                  (cudaStream_t)stream, d_out);
 }
@@ -1016,6 +1085,7 @@ int twb_twed_dev_f32(const float* dA, int64_t nA, const float* dTA, const float*
                      void* stream, double* d_out) {
     int rc = check_params(nA, nB, dim, nu, lam, degree);
     if (rc) return rc;
+    if (!dA || !dTA || !dB || !dTB || !d_out) return fail(TWB_EINVAL, "null pointer argument");
     return twed_pair_dev<float, float, double>(dA, nA, dTA, dB, nB, dTB, dim, nu, lam, degree,
                                                (cudaStream_t)stream, d_out);
 }
@@ -1094,7 +1164,7 @@ int twb_band_solve_f64(const double* va, const double* ta, const double* dela, i
     for (int k = 0; k < 6; ++k)
         CK(cudaMemcpyAsync(d[k], h[k], sizeof(double) * n[k], cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(dflag, 0, sizeof(int), st));
-    const double lim = safe_limit<double>();
+    const double lim = safe_limit<double>(dim);
     for (int k = 0; k < 6; ++k) {
         const bool is_del = k == 2 || k == 5;  // del[0] = +inf by construction
         const bool is_val = k == 0 || k == 3;
@@ -1103,15 +1173,32 @@ int twb_band_solve_f64(const double* va, const double* ta, const double* dela, i
     }
     // the DP kernels' copy marks the virtual row 0 with +inf (COL0_BY_INF)
     static const double infs[4] = {HUGE_VAL, HUGE_VAL, HUGE_VAL, HUGE_VAL};
-    CK(cudaMemcpyAsync(d[0], infs, sizeof(double) * dim, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d[3], infs, sizeof(double) * dim, cudaMemcpyHostToDevice, st));
+    for (int k = 0; k < 2; ++k) {
+        double* v0 = d[3 * k];
+        for (int c = 0; c < dim; c += 4)
+            CK(cudaMemcpyAsync(v0 + c, infs, sizeof(double) * std::min(4, dim - c),
+                               cudaMemcpyHostToDevice, st));
+    }
+    double* vt[2] = {nullptr, nullptr};
+    if (use_dyn(dim)) {
+        vt[0] = sc.get_n<double>((na + 1) * dim);
+        vt[1] = sc.get_n<double>((nb + 1) * dim);
+        if (sc.failed) return fail(TWB_ENOMEM, "device allocation failed");
+        for (int k = 0; k < 2; ++k) {
+            const int64_t rows = k ? nb + 1 : na + 1;
+            dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((dim + 31) / 32));
+            transpose_kernel<double><<<grid, dim3(32, 8), 0, st>>>(d[3 * k], rows, dim, vt[k]);
+            ++t_launches;
+            CK(cudaGetLastError());
+        }
+    }
     int hflag = 0;
     CK(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     const Variant v = pick_variant(dim, degree, nu, 0.0, hflag != 0, lim);
     WaveProblem<double, double> pr;
-    pr.A = {d[0], d[1], d[2]};
-    pr.B = {d[3], d[4], d[5]};
+    pr.A = {d[0], d[1], d[2], vt[0], na + 1};
+    pr.B = {d[3], d[4], d[5], vt[1], nb + 1};
     pr.nA = na;
     pr.nB = nb;
     if (!v.E && nb > na) {

@@ -8,7 +8,7 @@ namespace twb {
 
 template <int D, typename R, typename Z>
 cudaError_t batch_d(int P, bool E, bool N1, const BatchArgs<R, Z>& a, int64_t max_rows,
-                    cudaStream_t st, LaunchCtx* ctx);
+                    const Alloc& alloc, cudaStream_t st, LaunchCtx* ctx);
 
 template <int D, typename R, typename Z>
 cudaError_t wave_d(int P, bool E, bool N1, const WaveProblem<R, Z>& pr, const Alloc& alloc,

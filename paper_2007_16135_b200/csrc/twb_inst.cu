@@ -23,8 +23,9 @@ namespace twb {
 #if defined(TWB_KIND_BATCH)
 template <>
 cudaError_t batch_d<TWB_D, TWB_R, TWB_Z>(int P, bool E, bool N1, const BatchArgs<TWB_R, TWB_Z>& a,
-                                         int64_t max_rows, cudaStream_t st, LaunchCtx* ctx) {
-#define CALL(p, e, n) run_batch<TWB_D, p, e, n, TWB_R, TWB_Z>(a, max_rows, st, ctx)
+                                         int64_t max_rows, const Alloc& alloc, cudaStream_t st,
+                                         LaunchCtx* ctx) {
+#define CALL(p, e, n) run_batch<TWB_D, p, e, n, TWB_R, TWB_Z>(a, max_rows, alloc, st, ctx)
     TWB_SWITCH
 #undef CALL
 }

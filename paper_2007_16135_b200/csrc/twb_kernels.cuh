@@ -50,13 +50,14 @@ __device__ __forceinline__ double lp_rt(const double* x, const double* y, int d,
 // values: (ntot, d) raw samples of all series back to back (T = double or
 // float; float is widened exactly). off: (nseries+1) sample offsets.
 // Outputs prepared rows o = i + k + 1 for sample i of series k, and the
-// virtual row off[k] + k.
+// virtual row off[k] + k. Vt (optional, runtime-d kernels): the values again,
+// dim-major with leading dimension ldt.
 template <typename T, typename R, typename Z>
 __global__ void prepare_kernel(const T* __restrict__ values, const T* __restrict__ times,
                                const int64_t* __restrict__ off, int64_t nseries, int64_t ntot,
                                int64_t uniform_n, int d, double nu, double lam, int p,
                                double virt, R* __restrict__ V, R* __restrict__ Tm,
-                               Z* __restrict__ Del) {
+                               Z* __restrict__ Del, R* __restrict__ Vt, int64_t ldt) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntot + nseries;
          i += stride) {
@@ -66,6 +67,8 @@ __global__ void prepare_kernel(const T* __restrict__ values, const T* __restrict
             // virt: 0 (the reference's zero vector) or +inf (DP kernels'
             // copy: marks the virtual column, LaneRows::COL0_BY_INF).
             for (int c = 0; c < d; ++c) V[o * d + c] = (R)virt;
+            if (Vt)
+                for (int c = 0; c < d; ++c) Vt[c * ldt + o] = (R)virt;
             Tm[o] = R(0);
             Del[o] = (Z)dinf();
             continue;
@@ -118,6 +121,10 @@ __global__ void prepare_kernel(const T* __restrict__ values, const T* __restrict
         gap = fabs(ti - tp);
         int64_t o = i + k + 1;
         for (int c = 0; c < d; ++c) V[o * d + c] = (R)values[i * d + c];
+        // dim-major copy (runtime-d kernels): consecutive threads write
+        // consecutive rows of each component, coalesced
+        if (Vt)
+            for (int c = 0; c < d; ++c) Vt[c * ldt + o] = (R)values[i * d + c];
         Tm[o] = (R)times[i];
         Del[o] = (Z)__dadd_rn(__dadd_rn(cost, __dmul_rn(nu, gap)), lam);  // core.py:233
     }
@@ -133,7 +140,7 @@ constexpr int MAX_CHUNK = 64;  // B series per task
 
 template <int D, typename R, typename Z>
 __host__ __device__ constexpr size_t batch_smem(int warps) {
-    return sizeof(ColRing<D, R, Z>) * warps + sizeof(int) * MAX_CHUNK * warps;
+    return (sizeof(ColRing<D, R, Z>) * warps + sizeof(int) * MAX_CHUNK * warps + 15) / 16 * 16;
 }
 
 template <typename R, typename Z>
@@ -155,6 +162,8 @@ struct BatchArgs {
     double nu;
     int p;
     unsigned long long* counter;
+    int dd;    // components per sample (D == 0 kernels)
+    R* arows;  // D == 0: per-warp global blocks for the A rows (null: shared memory)
 };
 
 // Lanes per A series: 16 when every row-side series has <= 128 samples (two
@@ -180,6 +189,26 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
     ColRing<D, R, Z>& ring = rings[warp];
     const Z INF = zinf<Z>();
     Lane L;
+    if constexpr (D == 0) {  // the warp's rows block: shared memory after the rings, or global
+        R* srows = reinterpret_cast<R*>(smem_raw + batch_smem<D, R, Z>(WARPS));
+        const size_t blk = (size_t)K * args.dd * 32;
+        L.dd = args.dd;
+        L.sa = (args.arows ? args.arows + ((size_t)blockIdx.x * WARPS + warp) * blk
+                           : srows + (size_t)warp * blk) + lane;
+    }
+    // d(r, j) of the K rows at column j of the task's column stream
+    auto col_dists = [&](int64_t c0, int j, R (&mn)[K], bool safe) {
+        if constexpr (D == 0) {
+            L.dists_dyn(args.B.vt + c0 + j, args.B.ldt, args.p, mn);
+        } else {
+            const int slot = j & (RING_COLS - 1);
+            R vb[D];
+#pragma unroll
+            for (int k = 0; k < D; ++k) vb[k] = ring.v[slot * D + k];
+            if (safe) L.dists_safe(vb, args.p, mn);
+            else L.dists(vb, args.p, mn);
+        }
+    };
 
     while (true) {
         unsigned long long task = 0;
@@ -247,9 +276,6 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
             const int j = s - hl;
             if (j >= 0 && j < ncols) {
                 const int slot = j & (RING_COLS - 1);
-                R vb[D];
-#pragma unroll
-                for (int k = 0; k < D; ++k) vb[k] = ring.v[slot * D + k];
                 const R tb = ring.t[slot];
                 const Z delb = ring.del[slot];
                 const bool col0 = pos == 0;
@@ -264,7 +290,9 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
                     }
                     mup = R(0);
                 }
-                zbot = L.step(vb, tb, delb, zup, mup, col0, args.nu, args.p, mbot, zpn);
+                R mn[K];
+                col_dists(c0, j, mn, false);
+                zbot = L.chain(mn, tb, delb, zup, mup, col0, args.nu, mbot, zpn);
                 if (++pos == curlen) series_end(j);
             }
         };
@@ -284,11 +312,8 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
                 {
                     const int j = s - hl;
                     const int slot = j & (RING_COLS - 1);
-                    R vb[D];
-#pragma unroll
-                    for (int k = 0; k < D; ++k) vb[k] = ring.v[slot * D + k];
                     R mn[K];
-                    L.dists_safe(vb, args.p, mn);
+                    col_dists(c0, j, mn, true);
                     tbj = ring.t[slot];
                     L.prep(mn, tbj, ring.del[slot], L.zupp, L.mupp, L.tbp, args.nu, pre);
                 }
@@ -307,11 +332,8 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
                         zbot = L.chain2(pre, zup);
                         mbot = L.mr[K - 1];
                         const int slot = (j + 1) & (RING_COLS - 1);
-                        R vb[D];
-#pragma unroll
-                        for (int k = 0; k < D; ++k) vb[k] = ring.v[slot * D + k];
                         R mn[K];
-                        L.dists_safe(vb, args.p, mn);
+                        col_dists(c0, j + 1, mn, true);
                         const R tbn = ring.t[slot];
                         L.prep(mn, tbn, ring.del[slot], zpn, mup, tbj, args.nu, pre);
                         tbj = tbn;
@@ -433,6 +455,8 @@ struct WaveArgs {
     long long* dbg;  // diagnostics (TWB_DBG_TIMES): per stripe start / input ready / end (ns)
     const int* gate;  // run only if (*gate & 1) == gate_want (device-side variant choice)
     int gate_want;
+    int dd;    // components per sample (D == 0 kernels)
+    R* arows;  // D == 0: per-warp global blocks for the A rows (null: shared memory)
 };
 
 __device__ __forceinline__ long long globaltimer() {
@@ -484,8 +508,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
     const int ncols = (int)(args.nB + 1);
     const int nsteps = (ncols + C - 1) / C + 31;
     Lane L;
-    if constexpr (wave_sa<D, R>())
+    if constexpr (D == 0) {
+        const size_t blk = (size_t)K * args.dd * 32;
+        L.dd = args.dd;
+        L.sa = (args.arows ? args.arows + ((size_t)b * WARPS + warp) * blk : srows + (size_t)warp * blk) +
+               lane;
+    } else if constexpr (wave_sa<D, R>()) {
         L.sa = srows + ((size_t)warp * K * Lane::RC::NCH * 32 + lane) * Lane::RC::EPC;
+    }
 
     const int64_t s_last = (args.nA - 1) / args.H;
     const int64_t loc_last = (args.nA - 1) - s_last * args.H;
@@ -647,10 +677,18 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             }
             publish(j);
         };
-        auto load_col = [&](int j, R (&vb)[D]) {
-            const int slot = j & (NC - 1);
+        // d(r, j) of the lane's K rows (staged column, or the dim-major copy)
+        auto col_dists = [&](int j, R (&mn)[K], bool safe) {
+            if constexpr (D == 0) {
+                L.dists_dyn(args.B.vt + j, args.B.ldt, args.p, mn);
+            } else {
+                const int slot = j & (NC - 1);
+                R vb[D];
 #pragma unroll
-            for (int k = 0; k < D; ++k) vb[k] = ring.v[slot * D + k];
+                for (int k = 0; k < D; ++k) vb[k] = ring.v[slot * D + k];
+                if (safe) L.dists_safe(vb, args.p, mn);
+                else L.dists(vb, args.p, mn);
+            }
         };
 
         Z zbot[C];
@@ -679,11 +717,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                 Z zpn = zup;
                 if (C * st + c < ncols) top_input(st, c, zup, mup, zpn);
                 if (j >= 0 && j < ncols) {
-                    R vb[D];
-                    load_col(j, vb);
                     const int slot = j & (NC - 1);
-                    zbot[c] = L.step(vb, ring.t[slot], ring.del[slot], zup, mup, j == 0, args.nu,
-                                     args.p, mbot[c], zpn);
+                    R mn[K];
+                    col_dists(j, mn, false);
+                    zbot[c] = L.chain(mn, ring.t[slot], ring.del[slot], zup, mup, j == 0, args.nu,
+                                      mbot[c], zpn);
                     if (owner && j == ncols - 1) args.out[0] = L.z_at(own_q);
                 }
             }
@@ -735,11 +773,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             R tbj = L.tbp;
             if (C * (st - lane) >= 0) {
                 const int j = C * (st - lane);
-                R vb[D];
-                load_col(j, vb);
                 const int slot = j & (NC - 1);
                 R mn[K];
-                L.dists_safe(vb, args.p, mn);
+                col_dists(j, mn, true);
                 tbj = ring.t[slot];
                 L.prep(mn, tbj, ring.del[slot], L.zupp, L.mupp, L.tbp, args.nu, pre);
             }
@@ -769,11 +805,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                             // z(0, 0) = 0 is the diagonal of cell (1, 1); the
                             // row-0 ring holds +inf (the row above column 0)
                             const Z zd0 = (top_boundary && lane == 0 && j == 0) ? Z(0) : zin[c];
-                            R vb[D];
-                            load_col(j + 1, vb);
                             const int slot = (j + 1) & (NC - 1);
                             R mn[K];
-                            L.dists_safe(vb, args.p, mn);
+                            col_dists(j + 1, mn, true);
                             const R tbn = ring.t[slot];
                             L.prep(mn, tbn, ring.del[slot], zd0, min_[c], tbj, args.nu, pre);
                             tbj = tbn;
@@ -782,11 +816,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                         zbot[c] = L.chain2(pre, zin[c]);
                         mbot[c] = L.mr[K - 1];
                         if (check && owner && j == ncols - 1) args.out[0] = L.z_at(own_q);
-                        R vb[D];
-                        load_col(j + 1, vb);
                         const int slot = (j + 1) & (NC - 1);
                         R mn[K];
-                        L.dists_safe(vb, args.p, mn);
+                        col_dists(j + 1, mn, true);
                         const R tbn = ring.t[slot];
                         L.prep(mn, tbn, ring.del[slot], zin[c], min_[c], tbj, args.nu, pre);
                         tbj = tbn;

@@ -72,6 +72,7 @@ struct WaveProblem {
     double nu;
     int p;
     Z* out;  // device, one value
+    int dd = 0;  // components per sample (used by the D == 0 kernels)
     CtaRing<R, Z>* ring = nullptr;  // multi-kernel ring (A, B, out, alloc, st per part)
     const int* gate = nullptr;      // device flag: run only if (*gate & 1) == gate_want
     int gate_want = 0;
@@ -83,14 +84,27 @@ struct WaveProblem {
 // atomic task counter. The host groups rows by batch_lanes(max_rows).
 constexpr int BATCH_WARPS = 4;
 constexpr int BATCH_KMAX = 8;
+// Runtime-d (D == 0) kernels keep each warp's A rows (K * d * 32 values) in
+// shared memory while the CTA's total stays within these budgets; larger
+// blocks go to per-warp global scratch (L1/L2-resident for moderate d).
+constexpr size_t DYN_BATCH_SMEM_MAX = 100 * 1024;  // keeps >= 2 CTAs per SM
+constexpr size_t DYN_WAVE_SMEM_MAX = 200 * 1024;
 
 template <int D, int P, bool E, bool N1, typename R, typename Z>
-cudaError_t run_batch(BatchArgs<R, Z> a, int64_t max_rows, cudaStream_t st, LaunchCtx* ctx) {
+cudaError_t run_batch(BatchArgs<R, Z> a, int64_t max_rows, const Alloc& alloc, cudaStream_t st,
+                      LaunchCtx* ctx) {
     int sms = 0, dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t smem = batch_smem<D, R, Z>(BATCH_WARPS);
-    auto go = [&](auto kern) -> cudaError_t {
+    auto go = [&](auto kern, int K) -> cudaError_t {
+        size_t smem = batch_smem<D, R, Z>(BATCH_WARPS);
+        bool rows_global = false;
+        if constexpr (D == 0) {
+            const size_t rows = (size_t)BATCH_WARPS * K * a.dd * 32 * sizeof(R);
+            rows_global = smem + rows > DYN_BATCH_SMEM_MAX;
+            if (!rows_global) smem += rows;
+        }
+        a.arows = nullptr;
         int occ = 0;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -101,15 +115,19 @@ cudaError_t run_batch(BatchArgs<R, Z> a, int64_t max_rows, cudaStream_t st, Laun
         int64_t grid = (int64_t)sms * occ;
         if (want < grid) grid = want;
         if (grid < 1) grid = 1;
+        if (rows_global) {
+            a.arows = (R*)alloc.get((size_t)grid * BATCH_WARPS * K * a.dd * 32 * sizeof(R));
+            if (!a.arows) return cudaErrorMemoryAllocation;
+        }
         ctx->before(st);
         kern<<<(unsigned)grid, BATCH_WARPS * 32, smem, st>>>(a);
         ctx->after(st);
         return cudaGetLastError();
     };
-    if (max_rows <= 16 * 2) return go(batch_kernel<D, 2, 16, P, E, N1, BATCH_WARPS, R, Z>);
-    if (max_rows <= 16 * 4) return go(batch_kernel<D, 4, 16, P, E, N1, BATCH_WARPS, R, Z>);
-    if (max_rows <= 16 * 8) return go(batch_kernel<D, 8, 16, P, E, N1, BATCH_WARPS, R, Z>);
-    if (max_rows <= 32 * 8) return go(batch_kernel<D, 8, 32, P, E, N1, BATCH_WARPS, R, Z>);
+    if (max_rows <= 16 * 2) return go(batch_kernel<D, 2, 16, P, E, N1, BATCH_WARPS, R, Z>, 2);
+    if (max_rows <= 16 * 4) return go(batch_kernel<D, 4, 16, P, E, N1, BATCH_WARPS, R, Z>, 4);
+    if (max_rows <= 16 * 8) return go(batch_kernel<D, 8, 16, P, E, N1, BATCH_WARPS, R, Z>, 8);
+    if (max_rows <= 32 * 8) return go(batch_kernel<D, 8, 32, P, E, N1, BATCH_WARPS, R, Z>, 8);
     return cudaErrorInvalidValue;
 }
 
@@ -119,7 +137,13 @@ template <int D, int K, int C, int P, bool E, bool N1, int W, int MINB, typename
 cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream_t st,
                          LaunchCtx* ctx) {
     auto kern = wave_kernel<D, K, C, P, E, N1, W, MINB, R, Z>;
-    const size_t smem = wave_smem<D, R, Z, C, K>(W);
+    size_t smem = wave_smem<D, R, Z, C, K>(W);
+    bool rows_global = false;  // D == 0: the A rows in per-warp global blocks
+    if constexpr (D == 0) {
+        const size_t rows = (size_t)W * 32 * K * pr.dd * sizeof(R);
+        rows_global = smem + rows > DYN_WAVE_SMEM_MAX;
+        if (!rows_global) smem += rows;
+    }
     // The parts of the ring: one (this device, this stream) unless pr.ring.
     std::vector<WavePart<R, Z>> parts;
     if (pr.ring) {
@@ -143,7 +167,8 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
         int share = 0;
         for (int r = 0; r < np; ++r) share += parts[r].device == parts[q].device;
         const int dv = parts[q].device;
-        int slots = dv >= 0 && dv < 64 ? slots_cache[dv].load(std::memory_order_relaxed) : 0;
+        // (runtime-d kernels: shared memory depends on d, no cache)
+        int slots = D == 0 || dv < 0 || dv >= 64 ? 0 : slots_cache[dv].load(std::memory_order_relaxed);
         if (slots <= 0) {
             int sms = 0, occ = 0;
             cudaError_t e = cudaSetDevice(dv);
@@ -176,7 +201,8 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
     // factor max(1, ws*K*F/400)^0.75, F ~ FP64 instructions per cell (fitted
     // to B200 sweeps, e.g. n = 100k: d = 1 best at 1024-row stripes, d = 3 at
     // 512; n = 300k d = 3 at 1024; n = 1M at 12 x 6 rows).
-    const double F = D == 1 ? 10.0 : D == 2 ? 20.0 : D == 3 ? 24.0 : 27.0;
+    const double F = D == 0 ? 3.0 * pr.dd + 12.0
+                     : D == 1 ? 10.0 : D == 2 ? 20.0 : D == 3 ? 24.0 : 27.0;
     for (int ws = W; ws >= 1; --ws) {
         if (ws_pin > 0 && ws != (ws_pin < W ? ws_pin : W)) continue;
         // above 4, whole multiples of 4 warps: one warp short on a
@@ -253,6 +279,12 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
         a.dbg = nullptr;
         a.gate = pr.gate;
         a.gate_want = pr.gate_want;
+        a.dd = pr.dd;
+        a.arows = nullptr;
+        if (rows_global) {
+            a.arows = (R*)pt.alloc.get((size_t)g * W * 32 * K * pr.dd * sizeof(R));
+            if (!a.arows) return cudaErrorMemoryAllocation;
+        }
     }
     for (int l = 0; l < nl; ++l) {  // the last CTA of each part feeds the next part's CTA 0
         const WaveArgs<R, Z>& nx = args[(l + 1) % nl];
@@ -268,6 +300,35 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
     // TWB_DBG_TIMES=<file>: per-stripe timestamps (single kernel; diagnostics, synchronises)
     const char* dbg_path = nl == 1 && !pr.ring ? getenv("TWB_DBG_TIMES") : nullptr;
     if (dbg_path) args[0].dbg = (long long*)alloc.get(sizeof(long long) * (4 + 2 * W) * (size_t)S);
+    // A ring over several kernels: part l's last CTA writes into part l+1's
+    // inbox and progress counters, which were allocated and zeroed on part
+    // l+1's stream. Every part's stream waits for all parts' set-up before
+    // any kernel of the ring starts.
+    if (nl > 1) {
+        std::vector<cudaEvent_t> ready(nl, nullptr);
+        cudaError_t e0 = cudaSuccess;
+        for (int l = 0; l < nl && e0 == cudaSuccess; ++l) {
+            const WavePart<R, Z>& pt = parts[live[l]];
+            cudaSetDevice(pt.device);
+            e0 = cudaEventCreateWithFlags(&ready[l], cudaEventDisableTiming);
+            if (e0 == cudaSuccess) e0 = cudaEventRecord(ready[l], pt.st);
+        }
+        for (int l = 0; l < nl && e0 == cudaSuccess; ++l) {
+            const WavePart<R, Z>& pt = parts[live[l]];
+            cudaSetDevice(pt.device);
+            for (int m = 0; m < nl && e0 == cudaSuccess; ++m)
+                if (m != l) e0 = cudaStreamWaitEvent(pt.st, ready[m], 0);
+        }
+        for (int l = 0; l < nl; ++l)
+            if (ready[l]) {
+                cudaSetDevice(parts[live[l]].device);
+                cudaEventDestroy(ready[l]);
+            }
+        if (e0 != cudaSuccess) {
+            cudaSetDevice(cur_dev);
+            return e0;
+        }
+    }
     // Cooperative launch: every CTA of a kernel is co-resident (CTA b spins on
     // CTA b-1); the kernels of a ring are launched in ring order.
     cudaError_t e = cudaSuccess;
@@ -302,6 +363,10 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
 }
 
 template <int D, int P, bool E, bool N1, typename R, typename Z>
+cudaError_t run_wave_static(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream_t st,
+                            LaunchCtx* ctx, int sms);
+
+template <int D, int P, bool E, bool N1, typename R, typename Z>
 cudaError_t run_wave(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream_t st,
                      LaunchCtx* ctx) {
     int sms = 0, dev = 0;
@@ -317,6 +382,22 @@ cudaError_t run_wave(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream
             sms += m / share;
         }
     }
+    if constexpr (D == 0) {
+        // runtime d: 8 warps; 4 rows per lane while the rows fit in shared
+        // memory, else 2
+        const size_t rows4 = (size_t)8 * 32 * 4 * pr.dd * sizeof(R);
+        if (wave_smem<D, R, Z, 1, 4>(8) + rows4 <= DYN_WAVE_SMEM_MAX)
+            return run_wave_cfg<D, 4, 1, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
+        return run_wave_cfg<D, 2, 1, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
+    } else {
+        return run_wave_static<D, P, E, N1, R, Z>(pr, alloc, st, ctx, sms);
+    }
+}
+
+// Compile-time d (1..4): the configuration by the row-side length.
+template <int D, int P, bool E, bool N1, typename R, typename Z>
+cudaError_t run_wave_static(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaStream_t st,
+                            LaunchCtx* ctx, int sms) {
     // TWB_WAVE_CFG pins a variant (tuning experiments; proven-safe modes):
     // k<rows per lane>w<warps per CTA>[c<columns per step>]
     if constexpr (!E) {

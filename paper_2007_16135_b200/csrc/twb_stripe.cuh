@@ -35,15 +35,21 @@ struct PreparedT {
     const R* v;    // (rows, D)
     const R* t;    // (rows)
     const Z* del;  // (rows)
+    // D == 0 (runtime dimension): the same values dim-major, element k of
+    // prepared row r at vt[k * ldt + r] (read column-wise by the DP kernels)
+    const R* vt = nullptr;
+    int64_t ldt = 0;
 };
 
 constexpr int RING_COLS = 128;  // per-warp column staging ring (4 blocks of 32)
 
 // Per-warp column staging ring of NC columns (power of 2, multiple of 32).
+// D == 0 (runtime dimension): values are not staged (read from the dim-major
+// copy), only times and deletion costs.
 template <int D, typename R, typename Z, int NC = RING_COLS>
 struct ColRing {
     static constexpr int N = NC;
-    R v[NC * D];
+    R v[D > 0 ? NC * D : 1];
     R t[NC];
     Z del[NC];
 };
@@ -63,13 +69,15 @@ __device__ __forceinline__ void stage_block(ColRing<D, R, Z, NC>& ring, const Pr
     const bool ok = j < ncols;
     const int64_t g = c0 + (ok ? j : 0);
     const int slot = (int)(j & (NC - 1));
-    const int base = (int)((blk * 32) & (NC - 1)) * D;
+    if constexpr (D > 0) {
+        const int base = (int)((blk * 32) & (NC - 1)) * D;
 #pragma unroll
-    for (int k = 0; k < D; ++k) {
-        const int e = lane + 32 * k;  // element of the block's 32*D words
-        const int64_t gj = blk * 32 + e / D;
-        const bool okk = gj < ncols;
-        cp_async_elem(&ring.v[base + e], B.v + (c0 + (okk ? gj : 0)) * D + (e % D), okk);
+        for (int k = 0; k < D; ++k) {
+            const int e = lane + 32 * k;  // element of the block's 32*D words
+            const int64_t gj = blk * 32 + e / D;
+            const bool okk = gj < ncols;
+            cp_async_elem(&ring.v[base + e], B.v + (c0 + (okk ? gj : 0)) * D + (e % D), okk);
+        }
     }
     cp_async_elem(&ring.t[slot], B.t + g, ok);
     cp_async_elem(&ring.del[slot], B.del + g, ok);
@@ -184,18 +192,32 @@ struct RowChunks {
     static constexpr int BYTES_PER_LANE_ROW = NCH * 16;
 };
 
+// D == 0: runtime dimension `dd` (any d >= 1). The lane's K rows of A live at
+// sa[(q * dd + k) * 32] -- the warp's block [row][component][32 lanes] in
+// shared memory, or in a per-warp global scratch block when it does not fit
+// (the same addressing through a generic pointer); times stay in registers.
+// Column values come from the dim-major copy (PreparedT::vt): element k of
+// the lane's column at bcol[k * ldt], so a warp's 32 consecutive columns are
+// one coalesced load per component, reused for the K rows.
+#ifndef TWB_DYN_PREFETCH
+#define TWB_DYN_PREFETCH 0
+#endif
 template <int D, int K, int P, bool EXACT_NAN, bool NU1, typename R, typename Z, bool SA = false>
 struct LaneRows {
     static constexpr bool F32 = sizeof(R) == 4;
-    static constexpr bool SPLIT_SQRT = !F32 && D >= 2 && P == 2;
+    static constexpr bool DYN = D == 0;
+    static constexpr int DV = DYN ? 1 : D;  // static extent of value arrays
+    static constexpr bool SPLIT_SQRT = !F32 && (D >= 2 || DYN) && P == 2;
     static constexpr bool COL0_BY_INF = !EXACT_NAN;
-    using RC = RowChunks<D, R>;
-    R a[SA ? 1 : K][D];
+    static_assert(!(DYN && SA), "runtime-d rows have their own layout");
+    using RC = RowChunks<DV, R>;
+    R a[(SA || DYN) ? 1 : K][DV];
     R ta[SA ? 1 : K];
-    R* sa = nullptr;  // SA: element (lane * EPC) of the warp's row block
+    R* sa = nullptr;  // SA: element (lane * EPC) of the warp's row block; DYN: see above
+    int dd = DV;      // DYN: components per sample
 
     // values and time of row slot q
-    __device__ __forceinline__ void row(int q, R (&v)[D], R& t) const {
+    __device__ __forceinline__ void row(int q, R (&v)[DV], R& t) const {
         if constexpr (SA) {
             R e[RC::NCH * RC::EPC];
 #pragma unroll
@@ -223,9 +245,13 @@ struct LaneRows {
         }
     }
     __device__ __forceinline__ R row_t(int q) const {
-        R v[D], t;
-        row(q, v, t);
-        return t;
+        if constexpr (DYN) {
+            return ta[q];
+        } else {
+            R v[D], t;
+            row(q, v, t);
+            return t;
+        }
     }
     Z da[K];
     Z zl[K];  // z(r, j-1)
@@ -245,7 +271,10 @@ struct LaneRows {
             const int64_t r = r0 + q;
             const bool ok = r <= n;
             const int64_t g = base + (ok ? r : 0);
-            if constexpr (SA) {
+            if constexpr (DYN) {
+                for (int k = 0; k < dd; ++k) sa[(q * dd + k) * 32] = ok ? A.v[g * dd + k] : R(0);
+                ta[q] = ok ? A.t[g] : R(0);
+            } else if constexpr (SA) {
                 R e[RC::NCH * RC::EPC];
 #pragma unroll
                 for (int k = 0; k < RC::NCH * RC::EPC; ++k) e[k] = R(0);
@@ -278,7 +307,7 @@ struct LaneRows {
     }
 
     // d(r, j) for the lane's K rows.
-    __device__ __forceinline__ void dists(const R (&vb)[D], int p, R (&mn)[K]) const {
+    __device__ __forceinline__ void dists(const R (&vb)[DV], int p, R (&mn)[K]) const {
         if constexpr (SPLIT_SQRT) {
             bool ok = true;
 #pragma unroll
@@ -318,6 +347,88 @@ struct LaneRows {
                 R av[D], t;
                 row(q, av, t);
                 mn[q] = dist<D, P, R>(av, vb, p);
+            }
+        }
+    }
+
+    // DYN: d(r, j) for the lane's K rows, lp_dist (_kernels.py:24-48) with a
+    // runtime dimension: d == 1 -> |x0 - y0|; p == 1 -> sequential sum of
+    // |diff|; p == 2 -> sqrt of the sequential sum of diff*diff (fp64: same
+    // association, correctly rounded root; fp32 mode: FMA sums, approximate
+    // root, as the static-d fp32 kernels); else binary-exponentiation powers
+    // and pow for the root. bcol = element 0 of column j in the dim-major copy.
+    __device__ __forceinline__ void dists_dyn(const R* __restrict__ bcol, int64_t ldt, int p,
+                                              R (&mn)[K]) const {
+        static_assert(DYN, "runtime-d rows only");
+        const int d = dd;
+#if TWB_DYN_PREFETCH > 0
+        // the column TWB_DYN_PREFETCH steps ahead into L1 (the warp's 32
+        // lanes cover consecutive columns: one or two lines per component)
+        for (int k = 0; k < d; ++k)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(bcol + TWB_DYN_PREFETCH + k * ldt));
+#endif
+        const R* ar[K];
+#pragma unroll
+        for (int q = 0; q < K; ++q) ar[q] = sa + (size_t)q * d * 32;
+        const int pp = P ? P : p;
+        if (d == 1) {
+            const R b = __ldg(bcol);
+#pragma unroll
+            for (int q = 0; q < K; ++q) mn[q] = F32 ? (R)fabsf((float)(ar[q][0] - b)) : (R)fabs((double)(ar[q][0] - b));
+            return;
+        }
+        if (pp == 1 || pp == 2) {
+            R acc[K];
+            {
+                const R b = __ldg(bcol);
+#pragma unroll
+                for (int q = 0; q < K; ++q) {
+                    const R df = ar[q][0] - b;
+                    if constexpr (F32) acc[q] = pp == 1 ? fabsf(df) : df * df;
+                    else acc[q] = pp == 1 ? fabs(df) : __dmul_rn(df, df);
+                }
+            }
+#pragma unroll 2
+            for (int k = 1; k < d; ++k) {
+                const R b = __ldg(bcol + k * ldt);
+#pragma unroll
+                for (int q = 0; q < K; ++q) {
+                    const R df = ar[q][k * 32] - b;
+                    if constexpr (F32) acc[q] = pp == 1 ? acc[q] + fabsf(df) : __fmaf_rn(df, df, acc[q]);
+                    else acc[q] = pp == 1 ? __dadd_rn(acc[q], fabs(df)) : __dadd_rn(acc[q], __dmul_rn(df, df));
+                }
+            }
+            if (pp == 1) {
+#pragma unroll
+                for (int q = 0; q < K; ++q) mn[q] = acc[q];
+            } else if constexpr (F32) {
+#pragma unroll
+                for (int q = 0; q < K; ++q) mn[q] = sqrt_approx<!EXACT_NAN>(acc[q]);
+            } else if constexpr (!EXACT_NAN) {
+                sqrt_fast0_k<K>(acc, mn);
+            } else {
+#pragma unroll
+                for (int q = 0; q < K; ++q) mn[q] = __dsqrt_rn(acc[q]);
+            }
+            return;
+        }
+        if constexpr (P == 0) {  // degree >= 3 (runtime degree, NaN-exact kernels only)
+            R acc[K];
+#pragma unroll
+            for (int q = 0; q < K; ++q) acc[q] = R(0);
+            for (int k = 0; k < d; ++k) {
+                const R b = __ldg(bcol + k * ldt);
+#pragma unroll
+                for (int q = 0; q < K; ++q) {
+                    const R df = ar[q][k * 32] - b;
+                    if constexpr (F32) acc[q] += __powf(fabsf(df), (float)pp);
+                    else acc[q] = __dadd_rn(acc[q], int_power(fabs(df), pp));
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < K; ++q) {
+                if constexpr (F32) mn[q] = __powf(acc[q], 1.0f / (float)pp);
+                else mn[q] = pow(acc[q], 1.0 / (double)pp);
             }
         }
     }
@@ -394,7 +505,7 @@ struct LaneRows {
     // Straight-line distances (fp64 safe mode: sqrt_fast0, no branch; the
     // +inf virtual column gives NaN distances there, which only ever meet
     // z_diag = +inf and lose every min: pre = del_b, as with +inf).
-    __device__ __forceinline__ void dists_safe(const R (&vb)[D], int p, R (&mn)[K]) const {
+    __device__ __forceinline__ void dists_safe(const R (&vb)[DV], int p, R (&mn)[K]) const {
         if constexpr (SPLIT_SQRT) {
             double acc[K];
 #pragma unroll
@@ -464,7 +575,7 @@ struct LaneRows {
         return zu;
     }
 
-    __device__ __forceinline__ Z step(const R (&vb)[D], R tb, Z delb, Z zup, R mup, bool col0,
+    __device__ __forceinline__ Z step(const R (&vb)[DV], R tb, Z delb, Z zup, R mup, bool col0,
                                       double nu, int p, R& mbot, Z zupp_next) {
         R mn[K];
         dists(vb, p, mn);

@@ -13,7 +13,8 @@ and runs the sweep through ``twb_band_solve_f64`` (include/twb.h). ``install``
 swaps it into a ``twedband`` module so every reference caller -- warpband.twed,
 twedband.twed_parallel, twedband.twed_batch, the CLI -- runs on the GPU, and
 the reference's own test-suite can be pointed at the GPU kernel unchanged
-(tests/ref_seam_plugin.py, scripts/run_reference_suite.sh).
+(scripts/ref_seam_plugin.py, scripts/run_reference_suite.sh,
+tests/test_gpu_reference_suite.py).
 
 ``z``, ``z1``, ``z2`` are the reference's scratch diagonals; the GPU sweep
 keeps its band on the device and does not touch them (the value returned is

@@ -39,6 +39,44 @@ def small_golden():
 
 
 @pytest.fixture(scope="session")
+def wide_golden():
+    """Pairs and batches with d >= 5 (tests/golden/gen_wide.py, from the reference)."""
+    data = json.loads((GOLDEN / "wide.json").read_text())
+    data["matrices"] = dict(np.load(GOLDEN / "wide_batches.npz"))
+    return data
+
+
+def wide_pair_inputs(case):
+    """Regenerate a wide.json pair's inputs from its seeds."""
+    sys.path.insert(0, str(GOLDEN))
+    from series import seeded_pair
+    from paper_2007_16135_b200.workloads import make_pair
+    if "walk" in case:
+        w = case["walk"]
+        return make_pair(w["n"], w["d"], w["seed"])
+    return seeded_pair(case["inputs"])
+
+
+def wide_batch_inputs(spec):
+    """Regenerate a wide.json batch's (list_a, list_b) from its seeds."""
+    sys.path.insert(0, str(GOLDEN))
+    from series import ragged_set
+    from paper_2007_16135_b200.workloads import make_set
+    if spec["kind"] == "set":
+        S, T = make_set(spec["count"], spec["n"], spec["d"], spec["seed"])
+        return [(S[k], T[k]) for k in range(spec["count"])], None
+    la = ragged_set(spec["seed_a"], spec["lengths_a"], spec["d"])
+    lb = None if spec["seed_b"] is None else ragged_set(spec["seed_b"], spec["lengths_b"], spec["d"])
+    return la, lb
+
+
+def exact_expected(degree, d):
+    """fp64 bit-exact for degree 1/2 or d == 1; degree >= 3 with d >= 2: libm
+    pow vs CUDA pow decide the last bits (1e-12 relative)."""
+    return degree <= 2 or d == 1
+
+
+@pytest.fixture(scope="session")
 def config_golden():
     return json.loads((GOLDEN / "configs.json").read_text())
 

@@ -12,7 +12,8 @@ import math
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, as_values, dec, same_float
+from conftest import (GOLDEN, as_values, dec, exact_expected, same_float, wide_batch_inputs,
+                      wide_pair_inputs)
 from paper_2007_16135_b200.workloads import make_pair, make_set
 
 
@@ -133,3 +134,28 @@ def test_lcs_oracle_matches_reference_goldens():
         assert orc.lcs(s, t) == g["value"], g
     # generic hashable symbols share one code table (core.py:152-160, test_band.py:297)
     assert orc.lcs([1, "x", (2, 3), 4], ["x", (2, 3), 9]) == 2
+
+
+def test_wide_pairs_match_reference(wide_golden, oracle):
+    """d >= 5 (reference lp_dist over any m, _kernels.py:24-48): the oracle
+    against the reference's own values (tests/golden/gen_wide.py)."""
+    n_exact = 0
+    for case in wide_golden["pairs"]:
+        va, ta, vb, tb = wide_pair_inputs(case)
+        got = oracle.twed(va, ta, vb, tb, case["nu"], case["lam"], case["degree"])
+        want = float(dec(case["value"]))
+        if exact_expected(case["degree"], va.shape[1]):
+            assert same_float(got, want), (case["name"], got, want)
+            n_exact += 1
+        else:
+            assert got == pytest.approx(want, rel=1e-12), case["name"]
+    assert n_exact >= 60
+
+
+def test_wide_batches_match_reference(wide_golden, oracle):
+    for name, spec in wide_golden["batches"].items():
+        la, lb = wide_batch_inputs(spec)
+        got = oracle.twed_batch(la, lb, spec["nu"], spec["lam"], spec["degree"],
+                                spec["symmetric"])
+        want = wide_golden["matrices"][name]
+        assert got.shape == want.shape and np.array_equal(got, want), name
