@@ -61,6 +61,11 @@ _SIGS = {
                                           _i32, _pd]),
     "twb_prepare_series_f64": (ctypes.c_int, [_pd, _pd, _i64, _i32, _d, _d, _i32, _i32, _pd, _pd,
                                               _pd]),
+    "twb_prepare_pair_dev_f64": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _i64, _i32, _d, _d, _i32,
+                                                _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "twb_prepare_pair_dev_f32": (ctypes.c_int, [_vp, _vp, _i64, _vp, _vp, _i64, _i32, _d, _d, _i32,
+                                                _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "twb_trim_pool": (ctypes.c_int, [_i32]),
 }
 
 _lock = threading.Lock()

@@ -82,16 +82,18 @@ struct Scratch {
 };
 void* scratch_alloc(void* ctx, size_t n) { return ((Scratch*)ctx)->get(n); }
 
-// Keep freed scratch in the device's stream-ordered pool instead of returning
-// it to the driver at every synchronisation (the 1M pair uses ~1 GB of
-// boundary rows).
+// Keep up to 1 GB of freed scratch in the device's stream-ordered pool instead
+// of returning it to the driver at every synchronisation (a 1M pair's
+// prepared copies are ~150 MB; re-mapping them cost 12 ms per call and
+// 150-250 ms spikes). twb_trim_pool hands the cache back.
+constexpr uint64_t POOL_KEEP_BYTES = 1ull << 30;
 std::once_flag g_pool_once[64];
 void init_pool(int dev) {
     if (dev < 0 || dev >= 64) return;
     std::call_once(g_pool_once[dev], [dev]() {
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
+            uint64_t thr = POOL_KEEP_BYTES;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
         }
     });
@@ -186,23 +188,69 @@ int check_unsafe(const T* d, int64_t n, double limit, int* dflag, cudaStream_t s
     return 0;
 }
 
-// virt: value of the virtual row 0 of V -- 0 (the reference's layout) or
-// +inf (the DP kernels' marker of a virtual column, LaneRows::COL0_BY_INF).
-// Vt (optional): the dim-major copy for the runtime-d kernels, leading
-// dimension ntot + nseries (every prepared row).
+// The precompute of one or two segments (a pair's two series, or packed CSR
+// lists) in one launch, fused with the input check when flag != null
+// (twb_prepare.cuh). virt: value of the virtual row 0 of V -- 0 (the
+// reference's layout) or +inf (the DP kernels' marker of a virtual column,
+// LaneRows::COL0_BY_INF). Vt (optional): the dim-major copy for the
+// runtime-d kernels, leading dimension ntot + nseries (every prepared row).
+template <typename T, typename R, typename Z>
+struct PrepIn {
+    const T* v;
+    const T* t;
+    const int64_t* d_off;  // device offsets (null: uniform_n)
+    int64_t nseries, ntot, uniform_n;
+    R* V;
+    R* Tm;
+    Z* Del;
+    R* Vt;
+};
+template <typename T, typename R, typename Z>
+int prepare_fused(const PrepIn<T, R, Z>* in, int nseg, int dim, double nu, double lam, int degree,
+                  cudaStream_t st, double virt, int* flag, double limit, double tiny) {
+    PrepArgs<T, R, Z> a{};
+    int64_t tiles = 0;
+    for (int k = 0; k < nseg; ++k) {
+        PrepSeg<T, R, Z>& g = a.seg[k];
+        g.v = in[k].v;
+        g.t = in[k].t;
+        g.off = in[k].d_off;
+        g.nseries = in[k].nseries;
+        g.ntot = in[k].ntot;
+        g.uniform_n = in[k].uniform_n;
+        g.V = in[k].V;
+        g.Tm = in[k].Tm;
+        g.Del = in[k].Del;
+        g.Vt = in[k].Vt;
+        g.ldt = in[k].ntot + in[k].nseries;
+        g.tiles = (in[k].ntot + PREP_TILE - 1) / PREP_TILE;
+        tiles += g.tiles;
+    }
+    a.nseg = nseg;
+    a.d = dim;
+    a.nu = nu;
+    a.lam = lam;
+    a.p = degree;
+    a.virt = virt;
+    a.flag = flag;
+    a.limit = limit;
+    a.tiny = tiny;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // ~35 KB of staging per CTA: 6 CTAs per SM keep ~1.5k tile loads in flight
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms * 6));
+    prepare_kernel<T, R, Z><<<(unsigned)grid, PREP_TILE, 0, st>>>(a);
+    ++t_launches;
+    CK(cudaGetLastError());
+    return 0;
+}
 template <typename T, typename R, typename Z>
 int prepare(const T* values, const T* times, const int64_t* d_off, int64_t nseries, int64_t ntot,
             int64_t uniform_n, int dim, double nu, double lam, int degree, R* V, R* Tm, Z* Del,
             cudaStream_t st, double virt = HUGE_VAL, R* Vt = nullptr) {
-    const int64_t work = ntot + nseries;
-    int blocks = (int)std::min<int64_t>((work + 255) / 256, 148 * 16);
-    if (blocks < 1) blocks = 1;
-    prepare_kernel<T, R, Z><<<blocks, 256, 0, st>>>(values, times, d_off, nseries, ntot, uniform_n,
-                                                    dim, nu, lam, degree, virt, V, Tm, Del, Vt,
-                                                    work);
-    ++t_launches;
-    CK(cudaGetLastError());
-    return 0;
+    const PrepIn<T, R, Z> in{values, times, d_off, nseries, ntot, uniform_n, V, Tm, Del, Vt};
+    return prepare_fused<T, R, Z>(&in, 1, dim, nu, lam, degree, st, virt, nullptr, 0.0, 0.0);
 }
 
 // Launch bookkeeping for the next main-kernel launch: counts every launch
@@ -311,10 +359,6 @@ int twed_pair_dev(const T* dA, int64_t nA, const T* dTA, const T* dB, int64_t nB
     if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
     CK(cudaMemsetAsync(dflag, 0, sizeof(int), st));
     const double lim = safe_limit<R>(dim);
-    check_unsafe(dA, nA * dim, lim, dflag, st, safe_tiny<R>());
-    check_unsafe(dTA, nA, lim, dflag, st);
-    check_unsafe(dB, nB * dim, lim, dflag, st, safe_tiny<R>());
-    check_unsafe(dTB, nB, lim, dflag, st);
 
     const bool dyn = use_dyn(dim);
     R* V[2] = {sc.get_n<R>((nA + 1) * dim), sc.get_n<R>((nB + 1) * dim)};
@@ -328,12 +372,13 @@ int twed_pair_dev(const T* dA, int64_t nA, const T* dTA, const T* dB, int64_t nB
     Z* zout = sc.get_n<Z>(1);
     if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
     int rc;
-    if ((rc = prepare<T, R, Z>(dA, dTA, nullptr, 1, nA, nA, dim, nu, lam, degree, V[0], Tm[0],
-                               Del[0], st, HUGE_VAL, Vt[0])))
-        return rc;
-    if ((rc = prepare<T, R, Z>(dB, dTB, nullptr, 1, nB, nB, dim, nu, lam, degree, V[1], Tm[1],
-                               Del[1], st, HUGE_VAL, Vt[1])))
-        return rc;
+    {  // both series and the input check in one launch
+        const PrepIn<T, R, Z> in[2] = {{dA, dTA, nullptr, 1, nA, nA, V[0], Tm[0], Del[0], Vt[0]},
+                                       {dB, dTB, nullptr, 1, nB, nB, V[1], Tm[1], Del[1], Vt[1]}};
+        if ((rc = prepare_fused<T, R, Z>(in, 2, dim, nu, lam, degree, st, HUGE_VAL, dflag, lim,
+                                         safe_tiny<R>())))
+            return rc;
+    }
     const int64_t ldt[2] = {nA + 1, nB + 1};
     // No host round trip: the data-dependent choice between the proven-safe
     // sweep and the NaN-exact one is made on the device. Both are launched,
@@ -506,15 +551,11 @@ int twed_pair_multi(const T* A, int64_t nA, const T* TA, const T* B, int64_t nB,
         CK(cudaMemcpyAsync(dB, B, sizeof(T) * nB * dim, cudaMemcpyHostToDevice, pt.st));
         CK(cudaMemcpyAsync(dTB, TB, sizeof(T) * nB, cudaMemcpyHostToDevice, pt.st));
         CK(cudaMemsetAsync(pt.dflag, 0, sizeof(int), pt.st));
-        check_unsafe(dA, nA * dim, lim, pt.dflag, pt.st, safe_tiny<R>());
-        check_unsafe(dTA, nA, lim, pt.dflag, pt.st);
-        check_unsafe(dB, nB * dim, lim, pt.dflag, pt.st, safe_tiny<R>());
-        check_unsafe(dTB, nB, lim, pt.dflag, pt.st);
-        if ((rc = prepare<T, R, Z>(dA, dTA, nullptr, 1, nA, nA, dim, nu, lam, degree, pt.V[0],
-                                   pt.Tm[0], pt.Del[0], pt.st, HUGE_VAL, pt.Vt[0])))
-            return rc;
-        if ((rc = prepare<T, R, Z>(dB, dTB, nullptr, 1, nB, nB, dim, nu, lam, degree, pt.V[1],
-                                   pt.Tm[1], pt.Del[1], pt.st, HUGE_VAL, pt.Vt[1])))
+        const PrepIn<T, R, Z> in[2] = {
+            {dA, dTA, nullptr, 1, nA, nA, pt.V[0], pt.Tm[0], pt.Del[0], pt.Vt[0]},
+            {dB, dTB, nullptr, 1, nB, nB, pt.V[1], pt.Tm[1], pt.Del[1], pt.Vt[1]}};
+        if ((rc = prepare_fused<T, R, Z>(in, 2, dim, nu, lam, degree, pt.st, HUGE_VAL, pt.dflag, lim,
+                                         safe_tiny<R>())))
             return rc;
     }
     int hflag = 0;
@@ -631,22 +672,17 @@ int twed_batch_dev_impl(const T* dAA, const int64_t* a_off, int64_t nAA, const T
     }
     CK(cudaMemcpyAsync(d_bpoff, b_poff.data(), sizeof(int64_t) * (nBB + 1), cudaMemcpyHostToDevice, st));
     const double lim = safe_limit<R>(dim);
-    check_unsafe(dAA, totA * dim, lim, dflag, st, safe_tiny<R>());
-    check_unsafe(dTAA, totA, lim, dflag, st);
-    if (!self) {
-        check_unsafe(dBB, totB * dim, lim, dflag, st, safe_tiny<R>());
-        check_unsafe(dTBB, totB, lim, dflag, st);
+    int rc;
+    {  // both lists and the input check in one launch
+        const PrepIn<T, R, Z> in[2] = {
+            {dAA, dTAA, d_aoff, nAA, totA, uniform(a_off, nAA), VA, TmA, DelA, self ? VtB : nullptr},
+            {dBB, dTBB, d_boff, nBB, totB, uniform(b_off, nBB), VB, TmB, DelB, VtB}};
+        if ((rc = prepare_fused<T, R, Z>(in, self ? 1 : 2, dim, nu, lam, degree, st, HUGE_VAL, dflag,
+                                         lim, safe_tiny<R>())))
+            return rc;
     }
     int hflag = 0;
     CK(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, st));
-    int rc;
-    if ((rc = prepare<T, R, Z>(dAA, dTAA, d_aoff, nAA, totA, uniform(a_off, nAA), dim, nu, lam,
-                               degree, VA, TmA, DelA, st, HUGE_VAL, self ? VtB : nullptr)))
-        return rc;
-    if (!self &&
-        (rc = prepare<T, R, Z>(dBB, dTBB, d_boff, nBB, totB, uniform(b_off, nBB), dim, nu, lam,
-                               degree, VB, TmB, DelB, st, HUGE_VAL, VtB)))
-        return rc;
 
     // Output block: the kernel writes only solved entries (+ mirror).
     const bool mirror = tri && row_begin == 0 && row_end == nAA;
@@ -962,6 +998,25 @@ void api_count_launch() { ++t_launches; }
 LaunchCtx* api_ctx_begin() { return ctx_begin(); }
 }  // namespace twb
 
+// The single-pair precompute exactly as twb_twed_dev runs it (both series and
+// the input check in one launch), into caller buffers: the DP kernels' layout
+// (virtual row +inf). For timing and inspection of the HBM-bound precompute.
+template <typename T, typename R>
+int prepare_pair_dev(const T* A, const T* TA, int64_t nA, const T* B, const T* TB, int64_t nB,
+                     int dim, double nu, double lam, int degree, R* VA, R* TmA, double* DelA, R* VB,
+                     R* TmB, double* DelB, int* flag, void* stream) {
+    int rc = check_params(nA, nB, dim, nu, lam, degree);
+    if (rc) return rc;
+    if (!A || !TA || !B || !TB || !VA || !TmA || !DelA || !VB || !TmB || !DelB || !flag)
+        return fail(TWB_EINVAL, "null pointer argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const PrepIn<T, R, double> in[2] = {{A, TA, nullptr, 1, nA, nA, VA, TmA, DelA, nullptr},
+                                        {B, TB, nullptr, 1, nB, nB, VB, TmB, DelB, nullptr}};
+    CK(cudaMemsetAsync(flag, 0, sizeof(int), st));
+    return prepare_fused<T, R, double>(in, 2, dim, nu, lam, degree, st, HUGE_VAL, flag,
+                                       safe_limit<R>(dim), safe_tiny<R>());
+}
+
 extern "C" {
 
 int64_t twb_selftest_sqrt(int64_t n, uint64_t seed, int32_t device, int64_t* fast_count) {
@@ -1016,6 +1071,19 @@ double twb_probe_add_rate(int fp64, int device) {
 }
 
 int twb_version(void) { return 200; }
+
+int twb_trim_pool(int device) {
+    cudaMemPool_t pool;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, device);
+    if (e == cudaSuccess) e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaMemPoolTrimTo(pool, 0);
+    cudaSetDevice(cur);
+    if (e != cudaSuccess) return fail(TWB_ECUDA, "twb_trim_pool(%d): %s", device, cudaGetErrorString(e));
+    return TWB_OK;
+}
 
 size_t twb_last_error(char* buf, size_t len) {
     if (buf && len) {
@@ -1213,6 +1281,21 @@ int twb_band_solve_f64(const double* va, const double* ta, const double* dela, i
     CK(cudaMemcpyAsync(out, dout, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return 0;
+}
+
+int twb_prepare_pair_dev_f64(const double* A, const double* TA, int64_t nA, const double* B,
+                             const double* TB, int64_t nB, int32_t dim, double nu, double lam,
+                             int32_t degree, double* VA, double* TmA, double* DelA, double* VB,
+                             double* TmB, double* DelB, int32_t* unsafe_flag, void* stream) {
+    return prepare_pair_dev<double, double>(A, TA, nA, B, TB, nB, dim, nu, lam, degree, VA, TmA,
+                                            DelA, VB, TmB, DelB, unsafe_flag, stream);
+}
+int twb_prepare_pair_dev_f32(const float* A, const float* TA, int64_t nA, const float* B,
+                             const float* TB, int64_t nB, int32_t dim, double nu, double lam,
+                             int32_t degree, float* VA, float* TmA, double* DelA, float* VB,
+                             float* TmB, double* DelB, int32_t* unsafe_flag, void* stream) {
+    return prepare_pair_dev<float, float>(A, TA, nA, B, TB, nB, dim, nu, lam, degree, VA, TmA,
+                                          DelA, VB, TmB, DelB, unsafe_flag, stream);
 }
 
 int twb_prepare_series_f64(const double* values, const double* times, int64_t n, int32_t dim,

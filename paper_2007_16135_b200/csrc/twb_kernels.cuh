@@ -1,7 +1,8 @@
 // Kernels of the B200 TWED library (sm_100a).
 //
 //   prepare_kernel  : per-series precompute (core.py:218-234): zero-prefixed
-//                     values/times and deletion costs, HBM-bound.
+//                     values/times and deletion costs, HBM-bound, fused with
+//                     the input check (twb_prepare.cuh).
 //   batch_kernel    : all-pairs matrix (engine.py:183-226). One warp per task
 //                     (A series i, a run of B series); the warp keeps A's
 //                     rows in registers and streams the task's B series back
@@ -19,116 +20,10 @@
 //   (lcs_kernel, the bit-parallel LCS sweep, lives in twb_lcs.cu.)
 #pragma once
 
+#include "twb_prepare.cuh"
 #include "twb_stripe.cuh"
 
 namespace twb {
-
-// ---------------------------------------------------------------------------
-// Precompute. Runtime d and degree; same operation order as the reference.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double lp_rt(const double* x, const double* y, int d, int p) {
-    if (d == 1) return fabs(x[0] - y[0]);
-    if (p == 1) {
-        double acc = fabs(x[0] - y[0]);
-        for (int k = 1; k < d; ++k) acc = __dadd_rn(acc, fabs(x[k] - y[k]));
-        return acc;
-    }
-    if (p == 2) {
-        double d0 = x[0] - y[0];
-        double acc = __dmul_rn(d0, d0);
-        for (int k = 1; k < d; ++k) {
-            double dk = x[k] - y[k];
-            acc = __dadd_rn(acc, __dmul_rn(dk, dk));
-        }
-        return __dsqrt_rn(acc);
-    }
-    double acc = 0.0;
-    for (int k = 0; k < d; ++k) acc = __dadd_rn(acc, int_power(fabs(x[k] - y[k]), p));
-    return pow(acc, 1.0 / (double)p);
-}
-
-// values: (ntot, d) raw samples of all series back to back (T = double or
-// float; float is widened exactly). off: (nseries+1) sample offsets.
-// Outputs prepared rows o = i + k + 1 for sample i of series k, and the
-// virtual row off[k] + k. Vt (optional, runtime-d kernels): the values again,
-// dim-major with leading dimension ldt.
-template <typename T, typename R, typename Z>
-__global__ void prepare_kernel(const T* __restrict__ values, const T* __restrict__ times,
-                               const int64_t* __restrict__ off, int64_t nseries, int64_t ntot,
-                               int64_t uniform_n, int d, double nu, double lam, int p,
-                               double virt, R* __restrict__ V, R* __restrict__ Tm,
-                               Z* __restrict__ Del, R* __restrict__ Vt, int64_t ldt) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < ntot + nseries;
-         i += stride) {
-        if (i >= ntot) {  // virtual row of series k
-            int64_t k = i - ntot;
-            int64_t o = (uniform_n > 0 ? k * uniform_n : off[k]) + k;
-            // virt: 0 (the reference's zero vector) or +inf (DP kernels'
-            // copy: marks the virtual column, LaneRows::COL0_BY_INF).
-            for (int c = 0; c < d; ++c) V[o * d + c] = (R)virt;
-            if (Vt)
-                for (int c = 0; c < d; ++c) Vt[c * ldt + o] = (R)virt;
-            Tm[o] = R(0);
-            Del[o] = (Z)dinf();
-            continue;
-        }
-        int64_t k;
-        if (uniform_n > 0) {
-            k = i / uniform_n;
-        } else {  // last k with off[k] <= i
-            int64_t lo = 0, hi = nseries;
-            while (hi - lo > 1) {
-                int64_t mid = (lo + hi) >> 1;
-                if (off[mid] <= i) lo = mid; else hi = mid;
-            }
-            k = lo;
-        }
-        int64_t start = uniform_n > 0 ? k * uniform_n : off[k];
-        bool first = i == start;
-        double cur[16], prev[16];
-        double gap;
-        double cost;
-        double ti = (double)times[i];
-        double tp = first ? 0.0 : (double)times[i - 1];
-        if (d <= 16) {
-            for (int c = 0; c < d; ++c) {
-                cur[c] = (double)values[i * d + c];
-                prev[c] = first ? 0.0 : (double)values[(i - 1) * d + c];
-            }
-            cost = lp_rt(cur, prev, d, p);
-        } else {  // long vectors: same sums, read straight from memory
-            if (p == 1 || p == 2 || d == 1) {
-                double acc = 0.0;
-                for (int c = 0; c < d; ++c) {
-                    double x = (double)values[i * d + c];
-                    double y = first ? 0.0 : (double)values[(i - 1) * d + c];
-                    double df = x - y;
-                    double term = p == 1 ? fabs(df) : __dmul_rn(df, df);
-                    acc = c == 0 ? term : __dadd_rn(acc, term);
-                }
-                cost = p == 1 ? acc : __dsqrt_rn(acc);
-            } else {
-                double acc = 0.0;
-                for (int c = 0; c < d; ++c) {
-                    double x = (double)values[i * d + c];
-                    double y = first ? 0.0 : (double)values[(i - 1) * d + c];
-                    acc = __dadd_rn(acc, int_power(fabs(x - y), p));
-                }
-                cost = pow(acc, 1.0 / (double)p);
-            }
-        }
-        gap = fabs(ti - tp);
-        int64_t o = i + k + 1;
-        for (int c = 0; c < d; ++c) V[o * d + c] = (R)values[i * d + c];
-        // dim-major copy (runtime-d kernels): consecutive threads write
-        // consecutive rows of each component, coalesced
-        if (Vt)
-            for (int c = 0; c < d; ++c) Vt[c * ldt + o] = (R)values[i * d + c];
-        Tm[o] = (R)times[i];
-        Del[o] = (Z)__dadd_rn(__dadd_rn(cost, __dmul_rn(nu, gap)), lam);  // core.py:233
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Batch: all-pairs matrix.
@@ -430,12 +325,22 @@ struct WaveArgs {
     int64_t nA, nB;
     int64_t S;  // stripes
     int64_t H;  // rows per stripe
-    // Inboxes: slot b holds the bottom row (z, d / c) of the stripe above the
-    // one CTA b is sweeping, written by the CTA before it in the ring, and
-    // that producer's progress counter (stripe*(nB+1) + columns published).
-    Z* gbuf;            // gridDim.x x (nB+1)
-    R* gmbuf;           // gridDim.x x (nB+1)
+    // Inboxes: inbox b is a ring of rb columns holding the bottom row (z, d / c)
+    // of the stripe above the one CTA b is sweeping, written by the CTA before
+    // it in the ring, with that producer's progress counter
+    // (stripe*(nB+1) + columns published) and CTA b's consumption counter
+    // (round*(nB+1) + columns consumed, round = stripe / GT). Column j of the
+    // input of a round-r stripe sits in slot (r*(nB+1) + j) mod rb; the
+    // producer writes it once the consumer has passed index
+    // r*(nB+1) + j - rb (back-pressure), so scratch is O(G * rb), not
+    // O(G * nB). Progress of the whole ring needs GT * rb >= nB + 1 (every
+    // round's input fits in the ring before its consumer starts); the host
+    // picks rb >= 2 (nB + 1) / GT.
+    Z* gbuf;            // gridDim.x x rb
+    R* gmbuf;           // gridDim.x x rb
     long long* gprog;   // gridDim.x
+    long long* gcons;   // gridDim.x
+    int rbmask;         // rb - 1 (rb a power of 2)
     // The ring of CTAs may span several kernels (one per device, or several
     // on one device): this kernel's CTAs are ring positions cta0 .. cta0+G-1
     // of GT; stripe s belongs to ring position s % GT. The last CTA feeds the
@@ -445,6 +350,7 @@ struct WaveArgs {
     Z* next_z;
     R* next_m;
     long long* next_prog;
+    long long* next_cons;
     int sys;            // publish / poll the cross-kernel links at system scope
     int* abort;         // multi-kernel rings: set on a wait timeout (null: no timeout)
     long long timeout_ns;
@@ -551,12 +457,42 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         const bool owner = s == s_last && warp == own_warp && lane == own_lane;
         const long long gbase_in = (long long)(s - 1) * ncols;
         const long long gbase_out = (long long)s * ncols;
-        // own inbox in, the next ring position's inbox out
-        const Z* grow_in = args.gbuf + (int64_t)b * ncols;
-        const R* gmrow_in = args.gmbuf + (int64_t)b * ncols;
-        Z* grow_out = b + 1 < G ? args.gbuf + (int64_t)(b + 1) * ncols : args.next_z;
-        R* gmrow_out = b + 1 < G ? args.gmbuf + (int64_t)(b + 1) * ncols : args.next_m;
+        // own inbox in, the next ring position's inbox out (rings of rb columns)
+        const int64_t rb = (int64_t)args.rbmask + 1;
+        const Z* grow_in = args.gbuf + (int64_t)b * rb;
+        const R* gmrow_in = args.gmbuf + (int64_t)b * rb;
+        Z* grow_out = b + 1 < G ? args.gbuf + (int64_t)(b + 1) * rb : args.next_z;
+        R* gmrow_out = b + 1 < G ? args.gmbuf + (int64_t)(b + 1) * rb : args.next_m;
         long long* prog_out = b + 1 < G ? args.gprog + b + 1 : args.next_prog;
+        long long* cons_out = b + 1 < G ? args.gcons + b + 1 : args.next_cons;
+        // ring indices: this stripe's input is round s / GT of inbox b, its
+        // output round (s + 1) / GT of the next inbox
+        const long long ridx_in = (long long)(s / args.GT) * ncols;
+        const long long ridx_out = (long long)((s + 1) / args.GT) * ncols;
+        const int slot_in = (int)(ridx_in & args.rbmask);
+        const int slot_out = (int)(ridx_out & args.rbmask);
+        // output columns < room may be written (consumer's counter + rb)
+        long long room = 0;
+        auto wait_room = [&](long long jmax) {  // warp-uniform
+            if (jmax < room) return;
+            const long long t0 = args.abort ? now_ns() : 0;
+            while (true) {
+                const long long c = sys_out ? ld_acquire_sys(cons_out) : ld_acquire_gpu(cons_out);
+                room = c - ridx_out + rb;
+                if (jmax < room || TWB_DBG_NOSYNC >= 1) break;
+                if (args.abort) {  // multi-kernel ring: bounded wait
+                    if (*(volatile int*)args.abort || now_ns() - t0 > args.timeout_ns) {
+                        atomicExch_system(args.abort, 1);
+                        s_abort = 1;
+                        room = LLONG_MAX;
+                        break;
+                    }
+                }
+                __nanosleep(64);
+            }
+        };
+        if (top_boundary && warp == 0 && lane == 0)  // round 0 of inbox b has no input
+            publish_gpu(args.gcons + b, ridx_in + ncols, sys_in);
 
         // Previous stripe's bottom row (warp 0 of a non-top stripe): the 32C
         // columns of the next 32 steps are loaded into registers one block
@@ -577,9 +513,18 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
 #pragma unroll
             for (int k = 0; k < C; ++k) {
                 const int c = c0 + 32 * k + lane;
-                pz[k] = c < ncols ? __ldcg(grow_in + c) : Z(0);
-                pm[k] = c < ncols ? __ldcg(gmrow_in + c) : R(0);
+                const int slot = (slot_in + c) & args.rbmask;
+                pz[k] = c < ncols ? __ldcg(grow_in + slot) : Z(0);
+                pm[k] = c < ncols ? __ldcg(gmrow_in + slot) : R(0);
             }
+        };
+        // consumption counter of the own inbox: columns [0, c) are staged in
+        // shared memory (their loads have returned), the producer may reuse
+        // their slots; published every quarter ring and at the end
+        const int cons_gran = (args.rbmask + 1) >> 2;
+        auto consumed = [&](int c) {
+            if (lane == 0 && (c % cons_gran == 0 || c >= ncols))
+                publish_gpu(args.gcons + b, ridx_in + min(c, ncols), sys_in);
         };
         if (from_global) fetch(0);
         if (args.dbg && warp == 0 && lane == 0) args.dbg[s * 4 + 1] = globaltimer();
@@ -602,6 +547,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                         gstage[c % ZRS] = pz[k];
                         gmstage[c % ZRS] = pm[k];
                     }
+                    consumed(C * (st + 32));
                     if (C * (st + 32) < ncols) fetch(C * (st + 32));
                     __syncwarp();
                 }
@@ -670,9 +616,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                     mring[warp + 1][j % ZRS] = mb;
                 }
             } else if (to_global) {
+                wait_room(j);
                 if (lane == 31) {
-                    grow_out[j] = zb;
-                    gmrow_out[j] = mb;
+                    const int slot = (slot_out + j) & args.rbmask;
+                    grow_out[slot] = zb;
+                    gmrow_out[slot] = mb;
                 }
             }
             publish(j);
@@ -765,7 +713,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             // a dummy slot (last stripe's last warp); generic pointers
             Z* oz = to_ring ? zring[warp + 1] : (to_global ? grow_out : gstage);
             R* om = to_ring ? mring[warp + 1] : (to_global ? gmrow_out : gmstage);
-            const int omask = to_ring ? ZRS - 1 : (to_global ? 0x7fffffff : 0);
+            const int omask = to_ring ? ZRS - 1 : (to_global ? args.rbmask : 0);
+            const int obase = to_global ? slot_out : 0;
             const bool ow = lane == 31 && (to_ring || to_global);
             Z pre[K];
 #pragma unroll
@@ -830,8 +779,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                     // predicated, not branched: a lane-31-only branch makes
                     // every step a divergent region (BSSY/BSYNC + branch stalls)
                     const bool w = ow && (!check || j < ncols) && (!fill || j >= 0);
-                    st_pred(oz + (j & omask), zbot[c], w);
-                    st_pred(om + (j & omask), mbot[c], w);
+                    st_pred(oz + ((j + obase) & omask), zbot[c], w);
+                    st_pred(om + ((j + obase) & omask), mbot[c], w);
                 }
             };
             // full groups: lane 0's last column in the group is < ncols - 1
@@ -843,6 +792,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                     while (TWB_DBG_NOSYNC < 2 && ld_acquire_cta(&cons[warp + 1]) < need &&
                            !s_abort_seen())
                         spin_pause();
+                } else if (to_global) {
+                    wait_room(C * (st0 - 15) - 1);
                 }
                 if (st0 < 32) {
                     for (int i = 0; i < CHS; ++i) body(st0 + i, false, true);
@@ -866,6 +817,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             // drain: per-step flow control, lanes predicated on their columns
             for (; st < nsteps; ++st) {
                 preamble(st);
+                if (to_global) wait_room(C * (st - 30) - 1);
                 body(st, true, false);
 #pragma unroll
                 for (int c = 0; c < C; ++c) {

@@ -245,6 +245,17 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
     if (const char* env = getenv("TWB_WAVE_CHG")) chg = atoi(env);
     if (chg < 32 || (chg & (chg - 1))) chg = 32;
     const size_t ncols = (size_t)(pr.nB + 1);
+    // Inbox ring length (columns, power of 2): the ring of G CTAs progresses
+    // when G * rb >= ncols (WaveArgs); 2x margin, at least 4096 columns (far
+    // above the consumer's look-ahead and publish granularity), no more than
+    // a whole row. n = 1M on 145 CTAs: 16384 columns = 256 KB per inbox
+    // (37 MB in all, L2-resident) instead of 16 MB per inbox.
+    int64_t rb = 4096;
+    while (rb < (int64_t)ncols && rb * G < 2 * (int64_t)ncols) rb *= 2;
+    if (const char* env = getenv("TWB_WAVE_RB")) {  // tuning experiments
+        const int64_t v = atoll(env);
+        if (v >= 1024 && (v & (v - 1)) == 0 && v * G >= 2 * (int64_t)ncols) rb = v;
+    }
     std::vector<WaveArgs<R, Z>> args(nl);
     int64_t cta0 = 0;
     const int64_t pos_last = ((pr.nA - 1) / H) % G;  // ring position of the last stripe
@@ -263,11 +274,13 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
         a.p = pr.p;
         a.out = pt.out;
         const int64_t g = gp[live[l]];
-        a.gbuf = (Z*)pt.alloc.get(sizeof(Z) * (size_t)g * ncols);
-        a.gmbuf = (R*)pt.alloc.get(sizeof(R) * (size_t)g * ncols);
-        a.gprog = (long long*)pt.alloc.get(sizeof(long long) * (size_t)g);
+        a.rbmask = (int)(rb - 1);
+        a.gbuf = (Z*)pt.alloc.get(sizeof(Z) * (size_t)g * rb);
+        a.gmbuf = (R*)pt.alloc.get(sizeof(R) * (size_t)g * rb);
+        a.gprog = (long long*)pt.alloc.get(sizeof(long long) * 2 * (size_t)g);
         if (!a.gbuf || !a.gprog || !a.gmbuf) return cudaErrorMemoryAllocation;
-        cudaError_t e = cudaMemsetAsync(a.gprog, 0, sizeof(long long) * (size_t)g, pt.st);
+        a.gcons = a.gprog + g;
+        cudaError_t e = cudaMemsetAsync(a.gprog, 0, sizeof(long long) * 2 * (size_t)g, pt.st);
         if (e != cudaSuccess) return e;
         a.cta0 = cta0;
         a.GT = G;
@@ -291,6 +304,7 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
         args[l].next_z = nx.gbuf;
         args[l].next_m = nx.gmbuf;
         args[l].next_prog = nx.gprog;
+        args[l].next_cons = nx.gcons;
     }
     if (pr.gate == nullptr || pr.gate_want == 0) {  // the main sweep (not the gated NaN-exact one)
         ctx->wave_stripes = S;
