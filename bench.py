@@ -260,6 +260,16 @@ def run_reference(args, world, rank):
     for _ in range(args.steps):
         elapsed += solve(n)
     value = args.steps * n * n / elapsed / 1e9
+    # the rate at three sizes and the power-law fit t = c * n^a, extrapolated
+    # to the workload's n (the reference's CPU rate grows with n: the per-
+    # diagonal fork/join amortises)
+    sizes = [int(n / 2), int(n / 2 ** 0.5), n]
+    secs = [solve(sizes[0]), solve(sizes[1]), elapsed / args.steps]
+    a_fit, c_fit = np.polyfit(np.log(sizes), np.log(secs), 1)
+    t_full = float(np.exp(c_fit) * wl["n"] ** a_fit)
+    fit = {"n": sizes, "seconds": secs, "gcups": [x * x / t / 1e9 for x, t in zip(sizes, secs)],
+           "exponent": float(a_fit), "extrapolated_seconds_at_n": t_full,
+           "extrapolated_gcups_at_n": wl["n"] ** 2 / t_full / 1e9, "n_target": wl["n"]}
     from oracle import oracle as orc
     line = {
         "impl": "reference", "metric": METRIC, "value": value,
@@ -274,6 +284,7 @@ def run_reference(args, world, rank):
                          "host": orc.host_description()},
         "e2e": {"value": value, "unit": "GCUPS", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "fit": fit,
     }
     print(json.dumps(line), flush=True)
 
@@ -497,6 +508,11 @@ def run_extra(args, world, rank, local):
         res[name] = {"n": wl["n"], "d": wl["d"], "dtype": wl["dtype"], "kernel_ms": kms,
                      "gcups": wl["n"] * wl["n"] / (kms * 1e-3) / 1e9, "result": out.item()}
     res["lcs"] = run_lcs(args, world, rank, local)
+    res["precompute"] = run_precompute(args, local)
+    res["cfg1_host_latency"] = run_cfg1_latency(args, local)
+    res["mnist_shaped_d28"] = run_wide_batch(args, world, rank, local)
+    if world == 1:
+        res["batch_e2e"] = run_batch_e2e(args, local)
     # cfg4: AA 1000 x 256 (seed 3) against BB 1000 x 256 (seed 4), d = 1, fp64, full
     AA, TAA = make_set(1000, 256, 1, 3)
     BB, TBB = make_set(1000, 256, 1, 4)
@@ -517,6 +533,161 @@ def run_extra(args, world, rank, local):
                    "gcups": 1e6 * 256 * 256 / (kms * 1e-3) / 1e9, "n_gpus": world,
                    "sharding": "rows, no collective in the timed kernel"}
     return res
+
+
+def run_precompute(args, local):
+    """The single pair's precompute as twed_dev runs it (twb_prepare_pair_dev:
+    both cfg3 series, core.prepare_series C:218-234, fused with the input
+    check, bulk-copy staged tiles) timed alone with CUDA events, L2 flushed
+    before each launch. Achieved HBM GB/s = algorithmic bytes / time against
+    MEASURED_PEAKS.json hbm_gbs."""
+    import ctypes
+
+    import torch
+
+    from paper_2007_16135_b200 import _lib
+    from paper_2007_16135_b200.workloads import make_pair
+
+    lib = _lib.load()
+    dev = torch.device("cuda", local)
+    n, d = 1_000_000, 3
+    a, ta, b, tb = (torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in make_pair(n, d, 2))
+    V = [torch.empty((n + 1) * d, dtype=torch.float64, device=dev) for _ in range(2)]
+    T = [torch.empty(n + 1, dtype=torch.float64, device=dev) for _ in range(2)]
+    D = [torch.empty(n + 1, dtype=torch.float64, device=dev) for _ in range(2)]
+    flag = torch.zeros(1, dtype=torch.int32, device=dev)
+    l2 = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream(dev)
+
+    def launch():
+        _lib.check(lib.twb_prepare_pair_dev_f64(
+            a.data_ptr(), ta.data_ptr(), n, b.data_ptr(), tb.data_ptr(), n, d, 1.0, 1.0, 2,
+            V[0].data_ptr(), T[0].data_ptr(), D[0].data_ptr(), V[1].data_ptr(), T[1].data_ptr(),
+            D[1].data_ptr(), flag.data_ptr(), ctypes.c_void_p(st.cuda_stream)))
+
+    for _ in range(3):
+        launch()
+    times = []
+    for _ in range(20):
+        flush_l2(l2)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        launch()
+        e1.record(st)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    ms = float(np.median(times))
+    # per sample: reads d values + 1 time, writes d values + time + deletion cost
+    alg = 2 * n * ((d + 1) + (d + 2)) * 8 + 2 * (d + 2) * 8
+    peak = None
+    mp = REPO / "MEASURED_PEAKS.json"
+    if mp.exists():
+        try:
+            peak = float(json.loads(mp.read_text())["hbm_gbs"])
+        except (ValueError, KeyError):
+            peak = None
+    peak = peak or 6545.6
+    traffic = None
+    prof = REPO / "profiles" / "ncu_summary.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("prepare", {}).get("dram_bytes")
+        except (ValueError, AttributeError):
+            traffic = None
+    gbs = alg / (ms * 1e-3) / 1e9
+    return {"kernel": "twb::prepare_kernel (both cfg3 series + input check, one launch)",
+            "kernel_us": ms * 1e3, "algorithmic_bytes": alg, "achieved_gbs": gbs,
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                         "frac": gbs / peak, "traffic": traffic,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
+            "timing": "CUDA events around one launch, 256 MB L2 flush before each, median of 20",
+            "unsafe_flag": int(flag.item())}
+
+
+def run_cfg1_latency(args, local):
+    """Config 1 (n = 1000, d = 1, fp64) through the public host API, one call
+    at a time: numpy in, H2D, precompute, sweep, D2H of the distance."""
+    import paper_2007_16135_b200 as twb
+    from paper_2007_16135_b200.workloads import make_pair
+
+    a, ta, b, tb = make_pair(1_000, 1, 0)
+    for _ in range(5):
+        r = twb.twed(a, ta, b, tb, 1.0, 1.0, 2, device=local)
+    ts = []
+    for _ in range(50):
+        t0 = time.perf_counter()
+        r = twb.twed(a, ta, b, tb, 1.0, 1.0, 2, device=local)
+        ts.append(time.perf_counter() - t0)
+    return {"api": "paper_2007_16135_b200.twed (numpy in, float out)", "n": 1000, "d": 1,
+            "median_ms": float(np.median(ts)) * 1e3, "min_ms": float(np.min(ts)) * 1e3,
+            "calls": 50, "result": r, "e2e_gcups": 1e6 / float(np.median(ts)) / 1e9}
+
+
+def run_wide_batch(args, world, rank, local):
+    """The paper's R^28 shape (MNIST digits as 28 rows of 28 pixels,
+    PAPER.md:391): 2000 series of n = 28, d = 28, fp64, tri, device-resident,
+    through the runtime-d kernels (D = 0); the row blocks sharded over ranks."""
+    import torch
+
+    import paper_2007_16135_b200 as twb
+    from paper_2007_16135_b200 import _lib
+    from paper_2007_16135_b200.distributed import row_bounds
+    from paper_2007_16135_b200.workloads import make_set
+
+    lib = _lib.load()
+    lib.twb_set_kernel_timing(1)
+    dev = torch.device("cuda", local)
+    N, n, d = 2000, 28, 28
+    S, TS = make_set(N, n, d, 28)
+    dS = torch.from_numpy(np.ascontiguousarray(S.reshape(N * n, d))).to(dev)
+    dT = torch.from_numpy(np.ascontiguousarray(TS.reshape(N * n))).to(dev)
+    off = np.arange(N + 1, dtype=np.int64) * n
+    b0, b1 = row_bounds(N, world, True)[rank]
+    out = torch.empty((b1 - b0, N), dtype=torch.float64, device=dev)
+    ks = []
+    for _ in range(4):
+        twb.twed_batch_dev(dS, off, dT, nu=1.0, lamb=1.0, degree=2, tri=True, row_begin=b0,
+                           row_end=b1, out=out)
+        ks.append(lib.twb_last_kernel_ms())
+    kms = max_over_ranks(float(np.median(ks[1:])), world)
+    pairs = N * (N + 1) // 2
+    return {"series": N, "n": n, "d": d, "dtype": "f64", "layout": "tri", "pairs": pairs,
+            "kernel_ms": kms, "pairs_per_s": pairs / (kms * 1e-3),
+            "gcups": pairs * n * n / (kms * 1e-3) / 1e9, "kernel": "batch_kernel<D = 0> (runtime d)"}
+
+
+def run_batch_e2e(args, local):
+    """configs 4 and 5 through the public host API twed_batch: numpy in, the
+    validated lists packed, H2D, precompute, all-pairs kernel (+ on-device
+    mirror for tri), D2H of the whole matrix into numpy (8 MB / 400 MB)."""
+    import paper_2007_16135_b200 as twb
+    from paper_2007_16135_b200.workloads import make_set
+
+    out = {}
+    AA, TAA = make_set(1000, 256, 1, 3)
+    BB, TBB = make_set(1000, 256, 1, 4)
+    S, TS = make_set(10000, 128, 2, 5)
+    S32, TS32 = S.astype(np.float32), TS.astype(np.float32)
+    cases = {
+        "cfg4": (lambda: twb.twed_batch(AA, TAA, BB, TBB, 1.0, 1.0, 2, False, device=local),
+                 1000 * 1000, AA.nbytes + TAA.nbytes + BB.nbytes + TBB.nbytes, 8 * 10 ** 6),
+        "cfg5": (lambda: twb.twed_batch(S32, TS32, None, None, 1.0, 1.0, 2, True,
+                                        dtype=np.float32, device=local),
+                 10000 * 10001 // 2, S32.nbytes + TS32.nbytes, 4 * 10 ** 8),
+    }
+    for name, (call, pairs, h2d, d2h) in cases.items():
+        call()
+        ts = []
+        for _ in range(max(3, args.steps)):
+            t0 = time.perf_counter()
+            R = call()
+            ts.append(time.perf_counter() - t0)
+        dt = float(np.median(ts))
+        out[name] = {"api": "paper_2007_16135_b200.twed_batch (numpy in, numpy out)",
+                     "pairs": pairs, "ms": dt * 1e3, "pairs_per_s": pairs / dt,
+                     "h2d_bytes": int(h2d), "d2h_bytes": int(d2h), "shape": list(R.shape)}
+    return out
 
 
 def run_lcs(args, world, rank, local):
@@ -629,27 +800,28 @@ def run_batch_cfg5(args, world, rank, local):
     off = np.arange(N + 1, dtype=np.int64) * n
     bounds = row_bounds(N, world, True)
     b0, b1 = bounds[rank]
-    max_rows = max(e - b for b, e in bounds)
-    block = torch.zeros((max_rows, N), dtype=torch.float32, device=dev)
-    full = parts = None
-    if world > 1 and rank == 0:
-        full = torch.empty((N, N), dtype=torch.float32, device=dev)
-        parts = [torch.empty_like(block) for _ in range(world)]
+    # rank 0 solves straight into its rows of the full matrix; the others into
+    # their block, sent unpadded (exactly rows x N entries) to rank 0
+    full = torch.empty((N, N), dtype=torch.float32, device=dev) if rank == 0 else None
+    block = full[b0:b1] if rank == 0 else torch.empty((b1 - b0, N), dtype=torch.float32, device=dev)
     lib = _lib.load()
     lib.twb_set_kernel_timing(1)
 
     def step():
         twb.twed_batch_dev(dS, off, dT, nu=1.0, lamb=1.0, degree=2, tri=True, row_begin=b0,
-                           row_end=b1, out=block[: b1 - b0])
-        if world > 1:  # the job's only collective: gather the row blocks, mirror on rank 0
+                           row_end=b1, out=block)
+        if world > 1:  # the job's only exchange: the row blocks to rank 0, mirror there
             import torch.distributed as dist
-            dist.gather(block, parts, dst=0)
             if rank == 0:
-                for (lo, hi), part in zip(bounds, parts):
-                    full[lo:hi].copy_(part[: hi - lo])
+                reqs = [dist.irecv(full[lo:hi], src=r) for r, (lo, hi) in enumerate(bounds)
+                        if r > 0 and hi > lo]
+                for q in reqs:
+                    q.wait()
                 twb.mirror_upper_dev(full)
+            elif b1 > b0:
+                dist.send(block, dst=0)
 
-    for _ in range(max(1, args.warmup // 2)):
+    for _ in range(max(1, args.warmup)):
         step()
     torch.cuda.synchronize()
     barrier(world)
@@ -679,12 +851,106 @@ def run_batch_cfg5(args, world, rank, local):
             "gcups": cells / (ms * 1e-3) / 1e9, "ms_per_step": ms, "n_gpus": world,
             "scaling": "strong",
             "gather": ("none (one GPU: the kernel writes the mirrored matrix)" if world == 1 else
-                       "timed: NCCL gather of the row blocks to rank 0 + on-device mirror"),
+                       "timed: each rank's rows sent unpadded to rank 0 (NCCL send/recv, "
+                       f"{4 * N * (N - (bounds[0][1] - bounds[0][0]))} bytes in all) + "
+                       "on-device mirror"),
             "sharding": [list(b) for b in bounds],
             "kernel_ms": kms,
             "roofline": {"bound": "fp32", "achieved": FLOPS_PER_CELL[2] * cells / (kms * 1e-3) / 1e12,
                          "peak": peak / 1e12, "unit": "TFLOP/s",
                          "frac": FLOPS_PER_CELL[2] * cells / (kms * 1e-3) / peak}}
+
+
+BATCH_METRIC = "twed_batch pairs/s (tri 10k x 10k, n=128, d=2, fp32)"
+
+
+def run_ours_batch(args, world, rank, local):
+    """Headline at N > 1 (BASELINE: batch pairs/s on 1/2/4/8 GPUs): config 5
+    strong-scaled over the ranks, the unpadded gather to rank 0 and the
+    on-device mirror inside the timed region; e2e through
+    distributed.twed_batch_distributed (numpy in on every rank, numpy matrix
+    out on rank 0)."""
+    import torch
+
+    from paper_2007_16135_b200 import _lib
+    from paper_2007_16135_b200.distributed import twed_batch_distributed
+    from paper_2007_16135_b200.workloads import make_set
+
+    _lib.load()
+    _lib.require_device()
+    torch.cuda.set_device(local)
+    with ClockSampler(local) as clocks:
+        time.sleep(1.0)
+        _lib.take_launch_count()
+        clocks.mark_start()
+        batch = run_batch_cfg5(args, world, rank, local)
+        clocks.mark_end()
+    launches = _lib.take_launch_count()
+    N = args.batch_n
+    S, TS = make_set(N, 128, 2, 5)
+    S32, TS32 = S.astype(np.float32), TS.astype(np.float32)
+    twed_batch_distributed(S32, TS32, tri=True, dtype=np.float32)  # warm
+    barrier(world)
+    ts = []
+    for _ in range(max(1, args.steps)):
+        t0 = time.perf_counter()
+        R = twed_batch_distributed(S32, TS32, tri=True, dtype=np.float32)
+        ts.append(time.perf_counter() - t0)
+    e2e_s = max_over_ranks(float(np.median(ts)), world)
+    pairs = batch["pairs"]
+    if rank == 0:
+        assert R.shape == (N, N)
+        line = {
+            "metric": BATCH_METRIC, "value": batch["value"], "unit": "pairs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": batch["ms_per_step"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic random walks (SURVEY.md §8(d) make_set), unit timestamps",
+            "config": {"workload": "cfg5", "series": N, "n": 128, "d": 2, "layout": "tri",
+                       "nu": 1.0, "lam": 1.0, "degree": 2, "parallelism": f"row blocks x{world}",
+                       "l2": "400 MB output matrix written every step (> L2)"},
+            "e2e": {"value": pairs / e2e_s, "unit": "pairs/s",
+                    "h2d_bytes_per_step": int(world * (S32.nbytes + TS32.nbytes)),
+                    "d2h_bytes_per_step": int(4 * N * N), "ms_per_step": e2e_s * 1e3,
+                    "api": "paper_2007_16135_b200.distributed.twed_batch_distributed"},
+            "roofline": batch["roofline"] | {"kernel": "twb::batch_kernel", "kernel_ms": batch["kernel_ms"],
+                                             "flops_per_cell": FLOPS_PER_CELL[2]},
+            "cpu_baseline": None, "clocks": clocks.summary(), "gpu_launches": launches,
+            "batch": batch,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def run_reference_batch(args, world, rank):
+    """--impl reference for the batch headline: the reference's twed_batch
+    (engine.py:183-226) on all host cores, a bounded symmetric sample of
+    config 5 per step; rank 0 only."""
+    if rank != 0:
+        return
+    from paper_2007_16135_b200.workloads import make_set
+    threads = os.cpu_count() or 1
+    S, TS = make_set(args.batch_n, 128, 2, 5)
+    S = S.astype(np.float32).reshape(-1, 2)
+    TS = TS.astype(np.float32).reshape(-1)
+    res = batch_reference_rate(S, TS, 128, 2, count=240)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref not installed"}))
+        return
+    rates = [res["value"]]
+    for _ in range(max(0, args.steps - 1)):
+        rates.append(batch_reference_rate(S, TS, 128, 2, count=240)["value"])
+    value = float(np.mean(rates))
+    line = {"impl": "reference", "metric": BATCH_METRIC, "value": value, "unit": "pairs/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": res["seconds"] * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic random walks (SURVEY.md §8(d) make_set), fp32-rounded",
+            "config": {"workload": "cfg5", "series": args.batch_n, "n": 128, "d": 2,
+                       "sample_series": 240},
+            "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads,
+                             "kind": "reference", "sample": res["sample"]},
+            "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
 
 
 def main():
@@ -693,7 +959,9 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS) + ["cfg5"],
+                    help="default: cfg3 (the n = 1M pair) on one GPU, cfg5 (the sharded "
+                         "10k x 10k tri batch, BASELINE's 1/2/4/8-GPU metric) on several")
     ap.add_argument("--no-batch", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
@@ -704,13 +972,21 @@ def main():
     if args.warmup < 3:
         log("warning: fewer than 3 warm-up steps")
     world, rank, local = (1, 0, 0)
+    if args.workload is None:
+        args.workload = "cfg3" if int(os.environ.get("WORLD_SIZE", "1")) == 1 else "cfg5"
     if args.impl == "reference":
         world = int(os.environ.get("WORLD_SIZE", "1"))
         rank = int(os.environ.get("RANK", "0"))
-        run_reference(args, world, rank)
+        if args.workload == "cfg5":
+            run_reference_batch(args, world, rank)
+        else:
+            run_reference(args, world, rank)
         return
     world, rank, local = dist_setup()
-    run_ours(args, world, rank, local)
+    if args.workload == "cfg5":
+        run_ours_batch(args, world, rank, local)
+    else:
+        run_ours(args, world, rank, local)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

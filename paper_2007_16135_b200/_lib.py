@@ -51,6 +51,10 @@ _SIGS = {
                                           _i32, _i32, _i64, _i64, _i32, _pd]),
     "twb_twed_batch_f32": (ctypes.c_int, [_pf, _pi64, _i64, _pf, _pf, _pi64, _i64, _pf, _i32, _d, _d,
                                           _i32, _i32, _i64, _i64, _i32, _pf]),
+    "twb_twed_batch_multi_f64": (ctypes.c_int, [_pd, _pi64, _i64, _pd, _pd, _pi64, _i64, _pd, _i32,
+                                                _d, _d, _i32, _i32, _pi32, _i32, _pd]),
+    "twb_twed_batch_multi_f32": (ctypes.c_int, [_pf, _pi64, _i64, _pf, _pf, _pi64, _i64, _pf, _i32,
+                                                _d, _d, _i32, _i32, _pi32, _i32, _pf]),
     "twb_twed_batch_dev_f64": (ctypes.c_int, [_vp, _pi64, _i64, _vp, _vp, _pi64, _i64, _vp, _i32, _d,
                                               _d, _i32, _i32, _i64, _i64, _vp, _vp]),
     "twb_twed_batch_dev_f32": (ctypes.c_int, [_vp, _pi64, _i64, _vp, _vp, _pi64, _i64, _vp, _i32, _d,

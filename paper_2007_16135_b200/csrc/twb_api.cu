@@ -13,6 +13,7 @@
 #include <type_traits>
 #include <vector>
 #include <functional>
+#include <thread>
 
 #include "../../include/twb.h"
 #include "twb_dispatch.h"
@@ -918,6 +919,150 @@ int twed_batch_host(const T* AA, const int64_t* a_off, int64_t nAA, const T* TAA
     return 0;
 }
 
+// ---------------------------------------------------------------------------
+// All-pairs matrix over several devices in one call (SURVEY.md §8(b) C-ABI
+// form `devices, ndev`; §8(e) sharding): contiguous row blocks balanced by
+// work (pairs x row length; j >= i pairs for the triangle), one host thread
+// per device, no collective. Each device writes its rows straight into the
+// caller's matrix; for the triangle it also writes the mirror of its rows'
+// upper part: the diagonal square is mirrored on the device and the strip
+// right of it goes back transposed into the columns of its rows -- the
+// reference's mirror (engine.py:223-225) without a host pass over the matrix.
+// ---------------------------------------------------------------------------
+// m (rows x ld, row-major): the square [0, n) x [c0, c0 + n) mirrored, upper
+// -> lower (32x32 tiles through shared memory).
+template <typename T>
+__global__ void mirror_block_kernel(T* m, int64_t ld, int64_t c0, int64_t n) {
+    __shared__ T tile[32][33];
+    const int64_t bi = blockIdx.y, bj = blockIdx.x;
+    if (bj < bi) return;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t i = bi * 32 + r, j = bj * 32 + tx;
+        if (i < n && j < n) tile[r][tx] = m[i * ld + c0 + j];
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t j = bj * 32 + r, i = bi * 32 + tx;
+        if (i < n && j < n && j > i) m[j * ld + c0 + i] = tile[tx][r];
+    }
+}
+// dst (cols x rows) = transpose of src (rows x cols, leading dimension lds).
+template <typename T>
+__global__ void transpose_block_kernel(const T* __restrict__ src, int64_t lds, int64_t rows,
+                                       int64_t cols, T* __restrict__ dst) {
+    __shared__ T tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int64_t r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[i][threadIdx.x] = src[r * lds + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += 8) {
+        const int64_t c = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) dst[c * rows + r] = tile[threadIdx.x][i];
+    }
+}
+
+template <typename T, typename O>
+int twed_batch_multi(const T* AA, const int64_t* a_off, int64_t nAA, const T* TAA, const T* BB,
+                     const int64_t* b_off, int64_t nBB, const T* TBB, int dim, double nu, double lam,
+                     int degree, int tri, const int32_t* devices, int32_t ndev, O* out) {
+    const bool self = BB == nullptr;
+    int rc = check_batch(a_off, nAA, self ? nullptr : b_off, nBB, dim, nu, lam, degree, 0, nAA);
+    if (rc) return rc;
+    if (tri && !self) return fail(TWB_EINVAL, "symmetric=True requires both lists to be the same collection");
+    if (!AA || !TAA || !out || (!self && (!TBB || !b_off)) || !devices || ndev < 1)
+        return fail(TWB_EINVAL, "null pointer argument or empty device list");
+    int ndevs = 0;
+    CK(cudaGetDeviceCount(&ndevs));
+    for (int k = 0; k < ndev; ++k)
+        if (devices[k] < 0 || devices[k] >= ndevs)
+            return fail(TWB_EINVAL, "device %d out of range (%d devices)", devices[k], ndevs);
+    const int64_t ncols = self ? nAA : nBB;
+    if (ndev == 1)
+        return twed_batch_host<T, O>(AA, a_off, nAA, TAA, BB, b_off, nBB, TBB, dim, nu, lam, degree,
+                                     tri, 0, nAA, devices[0], out);
+    // row blocks of equal work: row i costs len_i * (sum of its columns' lengths)
+    const int64_t* coff = self ? a_off : b_off;
+    std::vector<double> suffix(ncols + 1, 0.0);  // column lengths summed from j on
+    for (int64_t j = ncols - 1; j >= 0; --j) suffix[j] = suffix[j + 1] + (double)(coff[j + 1] - coff[j]);
+    std::vector<double> w(nAA + 1, 0.0);
+    for (int64_t i = 0; i < nAA; ++i)
+        w[i + 1] = w[i] + (double)(a_off[i + 1] - a_off[i]) * (tri ? suffix[i] : suffix[0]);
+    std::vector<int64_t> lo(ndev + 1, 0);
+    for (int k = 1; k < ndev; ++k) {
+        const double target = w[nAA] * k / ndev;
+        lo[k] = std::max(lo[k - 1], (int64_t)(std::lower_bound(w.begin(), w.end(), target) - w.begin()));
+        lo[k] = std::min(lo[k], nAA);
+    }
+    lo[ndev] = nAA;
+    std::vector<int> rcs(ndev, 0);
+    std::vector<std::string> msgs(ndev);
+    auto block = [&](int k) -> int {
+        const int64_t r0 = lo[k], r1 = lo[k + 1];
+        if (r1 <= r0) return 0;
+        const int64_t rows = r1 - r0;
+        CK(cudaSetDevice(devices[k]));
+        init_pool(devices[k]);
+        cudaStream_t st = cudaStreamPerThread;
+        Scratch sc(st);
+        const int64_t totA = a_off[nAA], totB = self ? 0 : b_off[nBB];
+        T* dA = sc.get_n<T>(totA * dim);
+        T* dTA = sc.get_n<T>(totA);
+        T* dB = self ? nullptr : sc.get_n<T>(totB * dim);
+        T* dTB = self ? nullptr : sc.get_n<T>(totB);
+        O* dout = sc.get_n<O>((size_t)rows * ncols);
+        const int64_t strip = tri ? ncols - r1 : 0;  // columns right of the diagonal square
+        O* dtr = strip > 0 ? sc.get_n<O>((size_t)rows * strip) : nullptr;
+        if (sc.failed) return fail(TWB_ENOMEM, "device allocation failed on device %d", devices[k]);
+        CK(cudaMemcpyAsync(dA, AA, sizeof(T) * totA * dim, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dTA, TAA, sizeof(T) * totA, cudaMemcpyHostToDevice, st));
+        if (!self) {
+            CK(cudaMemcpyAsync(dB, BB, sizeof(T) * totB * dim, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(dTB, TBB, sizeof(T) * totB, cudaMemcpyHostToDevice, st));
+        }
+        int rc2 = twed_batch_dev<T, O>(dA, a_off, nAA, dTA, dB, b_off, nBB, dTB, dim, nu, lam, degree,
+                                       tri, r0, r1, st, dout);
+        if (rc2) return rc2;
+        if (!tri) {
+            CK(cudaMemcpyAsync(out + r0 * ncols, dout, sizeof(O) * (size_t)rows * ncols,
+                               cudaMemcpyDeviceToHost, st));
+        } else {
+            // the diagonal square, mirrored on the device
+            dim3 g1((unsigned)((rows + 31) / 32), (unsigned)((rows + 31) / 32));
+            mirror_block_kernel<O><<<g1, dim3(32, 8), 0, st>>>(dout, ncols, r0, rows);
+            ++t_launches;
+            CK(cudaGetLastError());
+            // rows r0..r1, columns r0.. (upper part + mirrored square)
+            CK(cudaMemcpy2DAsync(out + r0 * ncols + r0, sizeof(O) * ncols, dout + r0,
+                                 sizeof(O) * ncols, sizeof(O) * (ncols - r0), rows,
+                                 cudaMemcpyDeviceToHost, st));
+            if (strip > 0) {  // columns r1.. of these rows -> rows r1.. of columns r0..r1
+                dim3 g2((unsigned)((strip + 31) / 32), (unsigned)((rows + 31) / 32));
+                transpose_block_kernel<O><<<g2, dim3(32, 8), 0, st>>>(dout + r1, ncols, rows, strip, dtr);
+                ++t_launches;
+                CK(cudaGetLastError());
+                CK(cudaMemcpy2DAsync(out + r1 * ncols + r0, sizeof(O) * ncols, dtr, sizeof(O) * rows,
+                                     sizeof(O) * rows, strip, cudaMemcpyDeviceToHost, st));
+            }
+        }
+        CK(cudaStreamSynchronize(st));
+        return 0;
+    };
+    std::vector<std::thread> workers;
+    for (int k = 0; k < ndev; ++k)
+        workers.emplace_back([&, k]() {
+            DeviceGuard guard;
+            rcs[k] = block(k);
+            if (rcs[k]) msgs[k] = t_err;
+        });
+    for (auto& t : workers) t.join();
+    for (int k = 0; k < ndev; ++k)
+        if (rcs[k]) return fail(rcs[k], "device %d: %s", devices[k], msgs[k].c_str());
+    return 0;
+}
+
 template <typename T>
 int mirror_dev(T* d, int64_t n, cudaStream_t st) {
     if (!d || n < 1) return fail(TWB_EINVAL, "bad matrix");
@@ -1176,6 +1321,21 @@ int twb_twed_batch_f64(const double* AA, const int64_t* a_off, int64_t nAA, cons
                        int64_t row_begin, int64_t row_end, int32_t device, double* out) {
     return twed_batch_host<double, double>(AA, a_off, nAA, TAA, BB, b_off, nBB, TBB, dim, nu, lam,
                                            degree, tri, row_begin, row_end, device, out);
+}
+
+int twb_twed_batch_multi_f64(const double* AA, const int64_t* a_off, int64_t nAA, const double* TAA,
+                             const double* BB, const int64_t* b_off, int64_t nBB, const double* TBB,
+                             int32_t dim, double nu, double lam, int32_t degree, int32_t tri,
+                             const int32_t* devices, int32_t ndev, double* out) {
+    return twed_batch_multi<double, double>(AA, a_off, nAA, TAA, BB, b_off, nBB, TBB, dim, nu, lam,
+                                            degree, tri, devices, ndev, out);
+}
+int twb_twed_batch_multi_f32(const float* AA, const int64_t* a_off, int64_t nAA, const float* TAA,
+                             const float* BB, const int64_t* b_off, int64_t nBB, const float* TBB,
+                             int32_t dim, double nu, double lam, int32_t degree, int32_t tri,
+                             const int32_t* devices, int32_t ndev, float* out) {
+    return twed_batch_multi<float, float>(AA, a_off, nAA, TAA, BB, b_off, nBB, TBB, dim, nu, lam,
+                                          degree, tri, devices, ndev, out);
 }
 
 int twb_twed_batch_f32(const float* AA, const int64_t* a_off, int64_t nAA, const float* TAA,

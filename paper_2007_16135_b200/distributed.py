@@ -3,7 +3,8 @@
 SURVEY.md §8(e): the batch shards naturally (independent pairs). Every rank
 gets the whole input (it is tiny: <= 10 MB at the 10k x 10k config), solves a
 contiguous block of A rows on its own GPU with no collective, and the blocks
-are gathered to rank 0 -- the only collective. In tri mode (the reference's
+are gathered to rank 0 -- the only exchange: each rank sends exactly its rows
+(point to point, no padding) and rank 0 receives them into place. In tri mode (the reference's
 symmetric=True, engine.py:200-203, 223-225) each rank solves j >= i for its
 rows; rank 0 mirrors the strict upper triangle after the gather, on the device.
 
@@ -43,6 +44,14 @@ def row_bounds(n_rows: int, world: int, tri: bool, weights: Sequence[float] | No
     return [(bounds[r], bounds[r + 1]) for r in range(world)]
 
 
+def _global(group, r):
+    """Global rank of group rank r (send/recv address global ranks)."""
+    if group is None:
+        return r
+    import torch.distributed as dist
+    return dist.get_global_rank(group, r)
+
+
 def mirror_upper_numpy(m: np.ndarray) -> np.ndarray:
     iu = np.triu_indices(m.shape[0], k=1)
     m[(iu[1], iu[0])] = m[iu]
@@ -66,25 +75,31 @@ def sharded_batch(n_rows: int, n_cols: int, tri: bool,
     rank = dist.get_rank(group)
     bounds = row_bounds(n_rows, world, tri)
     b0, b1 = bounds[rank]
-    max_rows = max(e - b for b, e in bounds)
-    block = compute(b0, b1) if b1 > b0 else None
     if dtype is None:
         dtype = torch.float64
     if device is None:
         device = torch.device("cpu")
-    padded = torch.zeros((max_rows, n_cols), dtype=dtype, device=device)
-    if block is not None:
+
+    def as_tensor(block):
         t = block if isinstance(block, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(block))
-        padded[: b1 - b0].copy_(t.to(device=device, dtype=dtype))
+        return t.to(device=device, dtype=dtype).contiguous()
+
     if world == 1:
-        full = padded[:n_rows]
-    else:
-        gather_list = ([torch.empty_like(padded) for _ in range(world)]
-                       if rank == gather_to else None)
-        dist.gather(padded, gather_list, dst=gather_to, group=group)
-        if rank != gather_to:
-            return None
-        full = torch.cat([g[: e - b] for g, (b, e) in zip(gather_list, bounds)], dim=0)
+        return as_tensor(compute(0, n_rows))
+    # Gather without padding: every rank sends exactly its rows (point to
+    # point); rank `gather_to` receives each block straight into its rows of
+    # the full matrix -- rows x n_cols entries move per rank, nothing more.
+    if rank != gather_to:
+        if b1 > b0:
+            dist.send(as_tensor(compute(b0, b1)), dst=_global(group, gather_to), group=group)
+        return None
+    full = torch.empty((n_rows, n_cols), dtype=dtype, device=device)
+    reqs = [dist.irecv(full[lo:hi], src=_global(group, r), group=group)
+            for r, (lo, hi) in enumerate(bounds) if r != rank and hi > lo]
+    if b1 > b0:
+        full[b0:b1].copy_(as_tensor(compute(b0, b1)))
+    for q in reqs:
+        q.wait()
     if tri and world > 1:
         if full.is_cuda:
             from .api import mirror_upper_dev

@@ -35,12 +35,26 @@ if has launches; then
     > gpurun_out/${TAG}_ncu_launch_bench.log 2>&1
   echo "ncu launches exit $?" >> gpurun_out/${TAG}_ncu_launch_bench.log
 fi
+# every section of --set full except SourceCounters (its SASS instrumentation
+# slows a 2 s launch past any timeout; the source view comes from ncu_wave_src)
+FULL_NO_SRC="--section SpeedOfLight --section ComputeWorkloadAnalysis --section InstructionStats \
+  --section LaunchStats --section Occupancy --section SchedulerStats --section WarpStateStats \
+  --section MemoryWorkloadAnalysis --section MemoryWorkloadAnalysis_Chart \
+  --section MemoryWorkloadAnalysis_Tables --section SpeedOfLight_RooflineChart --section WorkloadDistribution"
 if has ncu_wave; then
   # the benchmarked cfg3 launch itself: no configuration overrides
-  timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+  timeout 1500 ncu $FULL_NO_SRC --metrics dram__bytes_read.sum,dram__bytes_write.sum \
+    --clock-control none --kernel-name-base demangled \
     -k "$K_WAVE" -c 1 -o gpurun_out/${TAG}_wave_cfg3 -f python scripts/prof_one.py cfg3 \
     > gpurun_out/${TAG}_ncu_wave.log 2>&1
   echo "ncu wave exit $?" >> gpurun_out/${TAG}_ncu_wave.log
+fi
+if has ncu_wave_src; then
+  # source-level counters on the same kernel configuration at n = 400k (one round of stripes)
+  TWB_WAVE_CFG=k6w12 TWB_WAVE_WS=12 timeout 1200 ncu --set full --clock-control none --import-source on \
+    --kernel-name-base demangled -k "$K_WAVE" -c 1 -o gpurun_out/${TAG}_wave_k6w12_n400k -f \
+    python scripts/prof_one.py cfg3 --n 400000 > gpurun_out/${TAG}_ncu_wave_src.log 2>&1
+  echo "ncu wave src exit $?" >> gpurun_out/${TAG}_ncu_wave_src.log
 fi
 if has ncu_batch; then
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:batch_kernel -c 1 \

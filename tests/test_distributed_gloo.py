@@ -22,7 +22,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, tri, q):
+def _worker(rank, world, port, tri, q, count=11):
     sys.path.insert(0, str(REPO))
     import torch.distributed as dist
 
@@ -34,7 +34,7 @@ def _worker(rank, world, port, tri, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     rng = np.random.default_rng(3)
     series = [(rng.standard_normal((int(n), 2)), np.arange(int(n), dtype=float))
-              for n in rng.integers(1, 40, size=11)]
+              for n in rng.integers(1, 40, size=count)]
 
     def compute(b0, b1):
         block = np.zeros((b1 - b0, len(series)))
@@ -51,12 +51,15 @@ def _worker(rank, world, port, tri, q):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("world,count", [(2, 11), (3, 11), (3, 2)])
 @pytest.mark.parametrize("tri", [False, True])
-def test_sharded_batch_world2(tri):
+def test_sharded_batch(world, count, tri):
+    """Ragged series, unequal row blocks (and an empty block when there are
+    fewer rows than ranks); every rank sends exactly its rows to rank 0."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, tri, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, tri, q, count)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:

@@ -100,6 +100,23 @@ def test_batch_over_device_list(twb, tri):
         assert np.array_equal(one, two)
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_batch_multi_abi_triangle_written_on_device(twb, dtype):
+    """twb_twed_batch_multi_*: 4 row blocks of a 700-series ragged triangle;
+    each block writes its rows and the transposed mirror strip of its upper
+    part from the device (no host mirror pass). Equal to one device, and
+    exactly symmetric with a zero diagonal."""
+    rng = np.random.default_rng(71)
+    series = [np.cumsum(rng.standard_normal((int(n), 3)), axis=0)
+              for n in rng.integers(1, 260, 700)]
+    one = twb.twed_batch(series, None, None, None, 1.0, 0.5, 2, True, dtype=dtype)
+    four = twb.twed_batch(series, None, None, None, 1.0, 0.5, 2, True, dtype=dtype,
+                          device=[0, 0, 0, 0])
+    assert four.dtype == dtype
+    assert np.array_equal(one, four)
+    assert np.array_equal(four, four.T) and np.all(np.diag(four) == 0)
+
+
 @pytest.mark.parametrize("degree,d", [(1, 3), (3, 2), (2, 1), (2, 4)])
 def test_ring_other_degrees_and_dims(twb, degree, d):
     """Degree 1 (sums of |diff|), degree 3 (the NaN-exact compare chain with a

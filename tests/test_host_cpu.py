@@ -102,15 +102,20 @@ def test_symbols_documented_in_integration():
         assert s in text
 
 
-def test_blocked_mirror_matches_reference_mirror():
-    """The in-process multi-device batch mirrors the triangle in row blocks
-    (engine.py:223-225: out[j, i] = out[i, j] for i < j)."""
-    from paper_2007_16135_b200.api import _mirror_upper_blocked
-    from paper_2007_16135_b200.distributed import mirror_upper_numpy
-    rng = np.random.default_rng(0)
-    for n in (1, 2, 255, 256, 257, 1000):
-        m = rng.standard_normal((n, n))
-        a, b = m.copy(), m.copy()
-        _mirror_upper_blocked(a, block=256)
-        mirror_upper_numpy(b)
-        assert np.array_equal(a, b), n
+def test_stacked_batch_input_validated_in_one_pass():
+    """Stacked (N, n[, d]) batch inputs are validated with TimeSeries' rules
+    (C:37-62) in one vectorised pass and packed without per-series copies."""
+    from paper_2007_16135_b200 import api
+    from paper_2007_16135_b200.core import InvalidInputError
+    p = api._to_list(np.zeros((5, 7, 2)), None, "series_a", np.float64)
+    assert len(p) == 5 and p.d == 2 and p.values.shape == (35, 2)
+    assert list(p.off) == [0, 7, 14, 21, 28, 35]
+    assert np.array_equal(p.times[:7], np.arange(7.0))
+    T = np.tile(np.arange(7.0), (5, 1))
+    T[3, 4] = T[3, 3]
+    with pytest.raises(InvalidInputError, match="strictly increasing"):
+        api._to_list(np.zeros((5, 7)), T, "series_a", np.float64)
+    with pytest.raises(ValueError, match="timestamps shape"):
+        api._to_list(np.zeros((5, 7)), np.zeros((5, 6)), "series_a", np.float64)
+    with pytest.raises(InvalidInputError, match="at least one sample"):
+        api._to_list(np.zeros((5, 0, 2)), None, "series_a", np.float64)
