@@ -281,7 +281,10 @@ constexpr int WAVE_UNROLL = TWB_WAVE_UNROLL;
 #define TWB_DBG_NOSYNC 0
 #endif
 constexpr int ZRS = 256;  // shared-memory ring between consecutive warps (columns)
-constexpr int CHS = 16;   // warp-to-warp publish granularity (columns)
+#ifndef TWB_CHS
+#define TWB_CHS 16
+#endif
+constexpr int CHS = TWB_CHS;  // warp-to-warp publish granularity (columns)
 constexpr int CHG = 32;   // CTA-to-CTA read granularity (columns; publish = args.chg)
 constexpr int CHG_RAMP = 4096;  // publish every group for the first columns of a stripe
 
@@ -340,7 +343,16 @@ struct WaveArgs {
     R* gmbuf;           // gridDim.x x rb
     long long* gprog;   // gridDim.x
     long long* gcons;   // gridDim.x
-    int rbmask;         // rb - 1 (rb a power of 2)
+    // Ring lengths (powers of 2): the inbox of ring position 0 -- the link
+    // that wraps from the last stripe of a round to the first of the next,
+    // whose consumer is still busy with its previous stripe while the
+    // producer runs ahead by up to a whole row -- holds rb0 >= nB + 1
+    // columns; every other inbox, whose consumer trails its producer by the
+    // pipeline lag only, rb columns. Layout of a kernel's gbuf: with
+    // cta0 == 0, inbox 0 (rb0) then inboxes 1.. (rb each); otherwise
+    // inboxes 0.. (rb each).
+    int rbmask;         // rb - 1
+    int rbmask0;        // rb0 - 1
     // The ring of CTAs may span several kernels (one per device, or several
     // on one device): this kernel's CTAs are ring positions cta0 .. cta0+G-1
     // of GT; stripe s belongs to ring position s % GT. The last CTA feeds the
@@ -458,19 +470,25 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         const long long gbase_in = (long long)(s - 1) * ncols;
         const long long gbase_out = (long long)s * ncols;
         // own inbox in, the next ring position's inbox out (rings of rb columns)
-        const int64_t rb = (int64_t)args.rbmask + 1;
-        const Z* grow_in = args.gbuf + (int64_t)b * rb;
-        const R* gmrow_in = args.gmbuf + (int64_t)b * rb;
-        Z* grow_out = b + 1 < G ? args.gbuf + (int64_t)(b + 1) * rb : args.next_z;
-        R* gmrow_out = b + 1 < G ? args.gmbuf + (int64_t)(b + 1) * rb : args.next_m;
+        const int64_t rbs = (int64_t)args.rbmask + 1;
+        auto inbox_off = [&](int64_t bl) {  // offset of local inbox bl in this kernel's gbuf
+            return args.cta0 == 0 ? (bl == 0 ? 0 : args.rbmask0 + 1 + (bl - 1) * rbs) : bl * rbs;
+        };
+        const int mask_in = (gb == 0) ? args.rbmask0 : args.rbmask;
+        const int mask_out = ((gb + 1) % args.GT == 0) ? args.rbmask0 : args.rbmask;
+        const int64_t rb = (int64_t)mask_out + 1;  // output ring length (room check)
+        const Z* grow_in = args.gbuf + inbox_off(b);
+        const R* gmrow_in = args.gmbuf + inbox_off(b);
+        Z* grow_out = b + 1 < G ? args.gbuf + inbox_off(b + 1) : args.next_z;
+        R* gmrow_out = b + 1 < G ? args.gmbuf + inbox_off(b + 1) : args.next_m;
         long long* prog_out = b + 1 < G ? args.gprog + b + 1 : args.next_prog;
         long long* cons_out = b + 1 < G ? args.gcons + b + 1 : args.next_cons;
         // ring indices: this stripe's input is round s / GT of inbox b, its
         // output round (s + 1) / GT of the next inbox
         const long long ridx_in = (long long)(s / args.GT) * ncols;
         const long long ridx_out = (long long)((s + 1) / args.GT) * ncols;
-        const int slot_in = (int)(ridx_in & args.rbmask);
-        const int slot_out = (int)(ridx_out & args.rbmask);
+        const int slot_in = (int)(ridx_in & mask_in);
+        const int slot_out = (int)(ridx_out & mask_out);
         // output columns < room may be written (consumer's counter + rb)
         long long room = 0;
         auto wait_room = [&](long long jmax) {  // warp-uniform
@@ -513,15 +531,16 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
 #pragma unroll
             for (int k = 0; k < C; ++k) {
                 const int c = c0 + 32 * k + lane;
-                const int slot = (slot_in + c) & args.rbmask;
+                const int slot = (slot_in + c) & mask_in;
                 pz[k] = c < ncols ? __ldcg(grow_in + slot) : Z(0);
                 pm[k] = c < ncols ? __ldcg(gmrow_in + slot) : R(0);
             }
         };
         // consumption counter of the own inbox: columns [0, c) are staged in
         // shared memory (their loads have returned), the producer may reuse
-        // their slots; published every quarter ring and at the end
-        const int cons_gran = (args.rbmask + 1) >> 2;
+        // their slots; published every 4096 columns (at most a quarter ring)
+        // and at the end
+        const int cons_gran = min((mask_in + 1) >> 2, 4096);
         auto consumed = [&](int c) {
             if (lane == 0 && (c % cons_gran == 0 || c >= ncols))
                 publish_gpu(args.gcons + b, ridx_in + min(c, ncols), sys_in);
@@ -618,7 +637,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             } else if (to_global) {
                 wait_room(j);
                 if (lane == 31) {
-                    const int slot = (slot_out + j) & args.rbmask;
+                    const int slot = (slot_out + j) & mask_out;
                     grow_out[slot] = zb;
                     gmrow_out[slot] = mb;
                 }
@@ -713,7 +732,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             // a dummy slot (last stripe's last warp); generic pointers
             Z* oz = to_ring ? zring[warp + 1] : (to_global ? grow_out : gstage);
             R* om = to_ring ? mring[warp + 1] : (to_global ? gmrow_out : gmstage);
-            const int omask = to_ring ? ZRS - 1 : (to_global ? args.rbmask : 0);
+            const int omask = to_ring ? ZRS - 1 : (to_global ? mask_out : 0);
             const int obase = to_global ? slot_out : 0;
             const bool ow = lane == 31 && (to_ring || to_global);
             Z pre[K];
@@ -787,13 +806,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             while (C * (st + CHS) < ncols) {
                 const int st0 = st;
                 preamble(st);
-                if (to_ring) {  // lane 31 writes columns < C*(st0 - 15) this group
-                    const int need = C * (st0 - 15) - ZRS;
+                if (to_ring) {  // lane 31 writes columns < C*(st0 + CHS - 31) this group
+                    const int need = C * (st0 + CHS - 31) - ZRS;
                     while (TWB_DBG_NOSYNC < 2 && ld_acquire_cta(&cons[warp + 1]) < need &&
                            !s_abort_seen())
                         spin_pause();
                 } else if (to_global) {
-                    wait_room(C * (st0 - 15) - 1);
+                    wait_room(C * (st0 + CHS - 31) - 1);
                 }
                 if (st0 < 32) {
                     for (int i = 0; i < CHS; ++i) body(st0 + i, false, true);

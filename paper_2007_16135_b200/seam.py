@@ -75,9 +75,32 @@ class Installed:
             setattr(self.kernels, name, fn)
 
 
-def install(twedband_module=None, device=0) -> Installed:
+class _Saved:
+    """Attributes replaced on several modules, restorable."""
+
+    def __init__(self):
+        self.items = []
+
+    def swap(self, module, name, fn):
+        self.items.append((module, name, getattr(module, name)))
+        setattr(module, name, fn)
+
+    def restore(self):
+        for module, name, fn in reversed(self.items):
+            setattr(module, name, fn)
+        self.items.clear()
+
+
+def install(twedband_module=None, device=0, batch=False) -> Installed:
     """Point ``twedband._kernels.twed_band_serial/_parallel`` (and
-    ``lcs_band_solve``) at the GPU sweeps."""
+    ``lcs_band_solve``) at the GPU sweeps.
+
+    batch=True also routes ``twedband.twed_batch`` / ``twedband.engine.twed_batch``
+    (E:183-226) to ONE all-pairs kernel launch on the GPU, instead of one
+    band-solve call (two host synchronisations) per pair: same entries, same
+    symmetric layout, the reference's DistanceMatrix. It is off by default
+    because the reference's own tests count the per-pair solver calls of its
+    batch (T/test_engine.py:127-128)."""
     if twedband_module is None:
         import twedband as twedband_module  # the reference package
     kernels = twedband_module._kernels
@@ -87,6 +110,31 @@ def install(twedband_module=None, device=0) -> Installed:
         names += ("lcs_band_solve",)
     saved = {name: getattr(kernels, name) for name in names}
     handle = Installed(kernels, saved)
+    if batch:
+        engine = twedband_module.engine
+        extra = _Saved()
+
+        def gpu_twed_batch(spec):
+            from .api import batch_matrix
+            from .core import TimeSeries, TwedParams
+            handle.calls += 1
+            mk = lambda lst: [TimeSeries(s.values, s.timestamps) for s in lst]  # noqa: E731
+            list_a = mk(spec.list_a)
+            list_b = None if spec.is_self_batch else mk(spec.list_b)
+            p = spec.params
+            out = batch_matrix(list_a, list_b, TwedParams(p.nu, p.lam, p.degree),
+                               symmetric=spec.symmetric, device=device)
+            return engine.DistanceMatrix(entries=out, symmetric=spec.symmetric)
+
+        extra.swap(engine, "twed_batch", gpu_twed_batch)
+        if getattr(twedband_module, "twed_batch", None) is not None:
+            extra.swap(twedband_module, "twed_batch", gpu_twed_batch)
+        base_restore = handle.restore
+
+        def restore():
+            extra.restore()
+            base_restore()
+        handle.restore = restore
 
     def gpu_band(z, z1, z2, va, ta, del_a, vb, tb, del_b, nu, p):
         handle.calls += 1

@@ -1,5 +1,5 @@
 """profiles/ncu_summary.json from an ncu DRAM-bytes capture of the cfg3 wave kernel
-(gpu_round.sh: dram__bytes_read.sum + dram__bytes_write.sum, one launch).
+(gpu_run.sh ncu_wave: dram__bytes_read.sum + dram__bytes_write.sum, one launch).
 
     python scripts/make_ncu_summary.py gpurun_out/<tag>_wave_cfg3_dram.csv
 """

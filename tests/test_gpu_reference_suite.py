@@ -58,3 +58,38 @@ def test_reference_bindings_tests_on_the_dropin_module():
     assert out.returncode == 0, tail + out.stderr[-2000:]
     assert "paper_2007_16135_b200.warpband" in tail, tail
     assert " passed" in tail and "failed" not in tail, tail
+
+
+def test_seam_batch_routing_one_launch():
+    """seam.install(batch=True): the reference's twed_batch (E:183-226) runs as
+    ONE all-pairs launch; entries and the symmetric layout equal the
+    reference's own CPU batch bit for bit (fp64), ragged lists included."""
+    code = r'''
+import sys, numpy as np
+import twedband as tb
+from paper_2007_16135_b200 import seam, _lib
+rng = np.random.default_rng(5)
+series = [tb.TimeSeries(np.cumsum(rng.standard_normal((int(n), 2)), axis=0),
+                        np.cumsum(rng.uniform(0.1, 2.0, int(n))))
+          for n in rng.integers(1, 200, 40)]
+other = [tb.TimeSeries(np.cumsum(rng.standard_normal((int(n), 2)), axis=0))
+         for n in rng.integers(1, 300, 17)]
+params = tb.TwedParams(0.5, 0.25, 2)
+want_sym = tb.twed_batch(tb.BatchSpec(series, series, params, symmetric=True, workers=4)).entries
+want_ab = tb.twed_batch(tb.BatchSpec(series, other, params, workers=4)).entries
+h = seam.install(tb, batch=True)
+_lib.take_launch_count()
+got_sym = tb.twed_batch(tb.BatchSpec(series, series, params, symmetric=True, workers=4))
+n_launch = _lib.take_launch_count()
+got_ab = tb.engine.twed_batch(tb.BatchSpec(series, other, params, workers=4)).entries
+h.restore()
+assert got_sym.symmetric and np.array_equal(got_sym.entries, want_sym)
+assert np.array_equal(got_ab, want_ab)
+assert h.calls == 2 and n_launch <= 4, (h.calls, n_launch)
+print("OK", n_launch)
+'''
+    env = dict(os.environ, NUMBA_CACHE_DIR="/tmp/twb_numba_cache",
+               PYTHONPATH=os.pathsep.join([str(REF), str(REPO)]))
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         timeout=600, cwd=str(REPO))
+    assert out.returncode == 0 and "OK" in out.stdout, out.stdout[-2000:] + out.stderr[-3000:]
