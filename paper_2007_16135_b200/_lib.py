@@ -94,7 +94,10 @@ def load():
                     "`python -c 'import __graft_entry__ as g; g.build()'` "
                     "(make -C paper_2007_16135_b200/csrc)")
             lib = ctypes.CDLL(str(path))
+            variant = "TWB_LIBRARY" in os.environ  # A/B builds may predate newer entry points
             for name, (res, args) in _SIGS.items():
+                if variant and not hasattr(lib, name):
+                    continue
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args

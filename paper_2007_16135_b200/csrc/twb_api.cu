@@ -83,11 +83,11 @@ struct Scratch {
 };
 void* scratch_alloc(void* ctx, size_t n) { return ((Scratch*)ctx)->get(n); }
 
-// Keep up to 1 GB of freed scratch in the device's stream-ordered pool instead
-// of returning it to the driver at every synchronisation (a 1M pair's
-// prepared copies are ~150 MB; re-mapping them cost 12 ms per call and
-// 150-250 ms spikes). twb_trim_pool hands the cache back.
-constexpr uint64_t POOL_KEEP_BYTES = 1ull << 30;
+// Keep up to 8 GB of freed scratch in the device's stream-ordered pool instead
+// of returning it to the driver at every synchronisation (a 1M pair's boundary
+// rows are 2.3 GB; re-mapping them cost 12 ms per call and 150-250 ms spikes).
+// twb_trim_pool hands the cache back.
+constexpr uint64_t POOL_KEEP_BYTES = 8ull << 30;
 std::once_flag g_pool_once[64];
 void init_pool(int dev) {
     if (dev < 0 || dev >= 64) return;
@@ -407,8 +407,13 @@ int twed_pair_dev(const T* dA, int64_t nA, const T* dTA, const T* dB, int64_t nB
         pr.out = zout;
         pr.gate = gate;
         pr.gate_want = want;
-        CK(call_wave<R, Z>(dim, v.P, v.E, v.N1, pr, sc, st));
-        if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
+        // The sweep's boundary rows come from their own scratch, returned to
+        // the stream-ordered pool right after the launch: the gated sweep that
+        // follows on the same stream reuses the same memory (one set of
+        // boundary rows per call, not two).
+        Scratch wsc(st);
+        CK(call_wave<R, Z>(dim, v.P, v.E, v.N1, pr, wsc, st));
+        if (wsc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
         return 0;
     };
     const Variant v_safe = pick_variant(dim, degree, nu, lam, false, lim);

@@ -281,10 +281,7 @@ constexpr int WAVE_UNROLL = TWB_WAVE_UNROLL;
 #define TWB_DBG_NOSYNC 0
 #endif
 constexpr int ZRS = 256;  // shared-memory ring between consecutive warps (columns)
-#ifndef TWB_CHS
-#define TWB_CHS 16
-#endif
-constexpr int CHS = TWB_CHS;  // warp-to-warp publish granularity (columns)
+constexpr int CHS = 16;   // warp-to-warp publish granularity (columns)
 constexpr int CHG = 32;   // CTA-to-CTA read granularity (columns; publish = args.chg)
 constexpr int CHG_RAMP = 4096;  // publish every group for the first columns of a stripe
 
@@ -328,31 +325,12 @@ struct WaveArgs {
     int64_t nA, nB;
     int64_t S;  // stripes
     int64_t H;  // rows per stripe
-    // Inboxes: inbox b is a ring of rb columns holding the bottom row (z, d / c)
-    // of the stripe above the one CTA b is sweeping, written by the CTA before
-    // it in the ring, with that producer's progress counter
-    // (stripe*(nB+1) + columns published) and CTA b's consumption counter
-    // (round*(nB+1) + columns consumed, round = stripe / GT). Column j of the
-    // input of a round-r stripe sits in slot (r*(nB+1) + j) mod rb; the
-    // producer writes it once the consumer has passed index
-    // r*(nB+1) + j - rb (back-pressure), so scratch is O(G * rb), not
-    // O(G * nB). Progress of the whole ring needs GT * rb >= nB + 1 (every
-    // round's input fits in the ring before its consumer starts); the host
-    // picks rb >= 2 (nB + 1) / GT.
-    Z* gbuf;            // gridDim.x x rb
-    R* gmbuf;           // gridDim.x x rb
+    // Inboxes: slot b holds the bottom row (z, d / c) of the stripe above the
+    // one CTA b is sweeping, written by the CTA before it in the ring, and
+    // that producer's progress counter (stripe*(nB+1) + columns published).
+    Z* gbuf;            // gridDim.x x (nB+1)
+    R* gmbuf;           // gridDim.x x (nB+1)
     long long* gprog;   // gridDim.x
-    long long* gcons;   // gridDim.x
-    // Ring lengths (powers of 2): the inbox of ring position 0 -- the link
-    // that wraps from the last stripe of a round to the first of the next,
-    // whose consumer is still busy with its previous stripe while the
-    // producer runs ahead by up to a whole row -- holds rb0 >= nB + 1
-    // columns; every other inbox, whose consumer trails its producer by the
-    // pipeline lag only, rb columns. Layout of a kernel's gbuf: with
-    // cta0 == 0, inbox 0 (rb0) then inboxes 1.. (rb each); otherwise
-    // inboxes 0.. (rb each).
-    int rbmask;         // rb - 1
-    int rbmask0;        // rb0 - 1
     // The ring of CTAs may span several kernels (one per device, or several
     // on one device): this kernel's CTAs are ring positions cta0 .. cta0+G-1
     // of GT; stripe s belongs to ring position s % GT. The last CTA feeds the
@@ -362,7 +340,6 @@ struct WaveArgs {
     Z* next_z;
     R* next_m;
     long long* next_prog;
-    long long* next_cons;
     int sys;            // publish / poll the cross-kernel links at system scope
     int* abort;         // multi-kernel rings: set on a wait timeout (null: no timeout)
     long long timeout_ns;
@@ -469,48 +446,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         const bool owner = s == s_last && warp == own_warp && lane == own_lane;
         const long long gbase_in = (long long)(s - 1) * ncols;
         const long long gbase_out = (long long)s * ncols;
-        // own inbox in, the next ring position's inbox out (rings of rb columns)
-        const int64_t rbs = (int64_t)args.rbmask + 1;
-        auto inbox_off = [&](int64_t bl) {  // offset of local inbox bl in this kernel's gbuf
-            return args.cta0 == 0 ? (bl == 0 ? 0 : args.rbmask0 + 1 + (bl - 1) * rbs) : bl * rbs;
-        };
-        const int mask_in = (gb == 0) ? args.rbmask0 : args.rbmask;
-        const int mask_out = ((gb + 1) % args.GT == 0) ? args.rbmask0 : args.rbmask;
-        const int64_t rb = (int64_t)mask_out + 1;  // output ring length (room check)
-        const Z* grow_in = args.gbuf + inbox_off(b);
-        const R* gmrow_in = args.gmbuf + inbox_off(b);
-        Z* grow_out = b + 1 < G ? args.gbuf + inbox_off(b + 1) : args.next_z;
-        R* gmrow_out = b + 1 < G ? args.gmbuf + inbox_off(b + 1) : args.next_m;
+        // own inbox in, the next ring position's inbox out
+        const Z* grow_in = args.gbuf + (int64_t)b * ncols;
+        const R* gmrow_in = args.gmbuf + (int64_t)b * ncols;
+        Z* grow_out = b + 1 < G ? args.gbuf + (int64_t)(b + 1) * ncols : args.next_z;
+        R* gmrow_out = b + 1 < G ? args.gmbuf + (int64_t)(b + 1) * ncols : args.next_m;
         long long* prog_out = b + 1 < G ? args.gprog + b + 1 : args.next_prog;
-        long long* cons_out = b + 1 < G ? args.gcons + b + 1 : args.next_cons;
-        // ring indices: this stripe's input is round s / GT of inbox b, its
-        // output round (s + 1) / GT of the next inbox
-        const long long ridx_in = (long long)(s / args.GT) * ncols;
-        const long long ridx_out = (long long)((s + 1) / args.GT) * ncols;
-        const int slot_in = (int)(ridx_in & mask_in);
-        const int slot_out = (int)(ridx_out & mask_out);
-        // output columns < room may be written (consumer's counter + rb)
-        long long room = 0;
-        auto wait_room = [&](long long jmax) {  // warp-uniform
-            if (jmax < room) return;
-            const long long t0 = args.abort ? now_ns() : 0;
-            while (true) {
-                const long long c = sys_out ? ld_acquire_sys(cons_out) : ld_acquire_gpu(cons_out);
-                room = c - ridx_out + rb;
-                if (jmax < room || TWB_DBG_NOSYNC >= 1) break;
-                if (args.abort) {  // multi-kernel ring: bounded wait
-                    if (*(volatile int*)args.abort || now_ns() - t0 > args.timeout_ns) {
-                        atomicExch_system(args.abort, 1);
-                        s_abort = 1;
-                        room = LLONG_MAX;
-                        break;
-                    }
-                }
-                __nanosleep(64);
-            }
-        };
-        if (top_boundary && warp == 0 && lane == 0)  // round 0 of inbox b has no input
-            publish_gpu(args.gcons + b, ridx_in + ncols, sys_in);
 
         // Previous stripe's bottom row (warp 0 of a non-top stripe): the 32C
         // columns of the next 32 steps are loaded into registers one block
@@ -531,19 +472,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
 #pragma unroll
             for (int k = 0; k < C; ++k) {
                 const int c = c0 + 32 * k + lane;
-                const int slot = (slot_in + c) & mask_in;
-                pz[k] = c < ncols ? __ldcg(grow_in + slot) : Z(0);
-                pm[k] = c < ncols ? __ldcg(gmrow_in + slot) : R(0);
+                pz[k] = c < ncols ? __ldcg(grow_in + c) : Z(0);
+                pm[k] = c < ncols ? __ldcg(gmrow_in + c) : R(0);
             }
-        };
-        // consumption counter of the own inbox: columns [0, c) are staged in
-        // shared memory (their loads have returned), the producer may reuse
-        // their slots; published every 4096 columns (at most a quarter ring)
-        // and at the end
-        const int cons_gran = min((mask_in + 1) >> 2, 4096);
-        auto consumed = [&](int c) {
-            if (lane == 0 && (c % cons_gran == 0 || c >= ncols))
-                publish_gpu(args.gcons + b, ridx_in + min(c, ncols), sys_in);
         };
         if (from_global) fetch(0);
         if (args.dbg && warp == 0 && lane == 0) args.dbg[s * 4 + 1] = globaltimer();
@@ -566,7 +497,6 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                         gstage[c % ZRS] = pz[k];
                         gmstage[c % ZRS] = pm[k];
                     }
-                    consumed(C * (st + 32));
                     if (C * (st + 32) < ncols) fetch(C * (st + 32));
                     __syncwarp();
                 }
@@ -635,11 +565,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                     mring[warp + 1][j % ZRS] = mb;
                 }
             } else if (to_global) {
-                wait_room(j);
                 if (lane == 31) {
-                    const int slot = (slot_out + j) & mask_out;
-                    grow_out[slot] = zb;
-                    gmrow_out[slot] = mb;
+                    grow_out[j] = zb;
+                    gmrow_out[j] = mb;
                 }
             }
             publish(j);
@@ -732,8 +660,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             // a dummy slot (last stripe's last warp); generic pointers
             Z* oz = to_ring ? zring[warp + 1] : (to_global ? grow_out : gstage);
             R* om = to_ring ? mring[warp + 1] : (to_global ? gmrow_out : gmstage);
-            const int omask = to_ring ? ZRS - 1 : (to_global ? mask_out : 0);
-            const int obase = to_global ? slot_out : 0;
+            const int omask = to_ring ? ZRS - 1 : (to_global ? 0x7fffffff : 0);
             const bool ow = lane == 31 && (to_ring || to_global);
             Z pre[K];
 #pragma unroll
@@ -798,21 +725,19 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                     // predicated, not branched: a lane-31-only branch makes
                     // every step a divergent region (BSSY/BSYNC + branch stalls)
                     const bool w = ow && (!check || j < ncols) && (!fill || j >= 0);
-                    st_pred(oz + ((j + obase) & omask), zbot[c], w);
-                    st_pred(om + ((j + obase) & omask), mbot[c], w);
+                    st_pred(oz + (j & omask), zbot[c], w);
+                    st_pred(om + (j & omask), mbot[c], w);
                 }
             };
             // full groups: lane 0's last column in the group is < ncols - 1
             while (C * (st + CHS) < ncols) {
                 const int st0 = st;
                 preamble(st);
-                if (to_ring) {  // lane 31 writes columns < C*(st0 + CHS - 31) this group
-                    const int need = C * (st0 + CHS - 31) - ZRS;
+                if (to_ring) {  // lane 31 writes columns < C*(st0 - 15) this group
+                    const int need = C * (st0 - 15) - ZRS;
                     while (TWB_DBG_NOSYNC < 2 && ld_acquire_cta(&cons[warp + 1]) < need &&
                            !s_abort_seen())
                         spin_pause();
-                } else if (to_global) {
-                    wait_room(C * (st0 + CHS - 31) - 1);
                 }
                 if (st0 < 32) {
                     for (int i = 0; i < CHS; ++i) body(st0 + i, false, true);
@@ -836,7 +761,6 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             // drain: per-step flow control, lanes predicated on their columns
             for (; st < nsteps; ++st) {
                 preamble(st);
-                if (to_global) wait_room(C * (st - 30) - 1);
                 body(st, true, false);
 #pragma unroll
                 for (int c = 0; c < C; ++c) {

@@ -245,20 +245,6 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
     if (const char* env = getenv("TWB_WAVE_CHG")) chg = atoi(env);
     if (chg < 32 || (chg & (chg - 1))) chg = 32;
     const size_t ncols = (size_t)(pr.nB + 1);
-    // Inbox rings (WaveArgs): ring position 0 -- the round-wrap link -- holds
-    // a whole row (rb0 >= ncols); the others rb columns, 4x the producer's
-    // lead over its consumer (pipeline lag of W warps, publish granularity,
-    // look-ahead), at least 8192. n = 1M on 145 CTAs: 16 MB + 144 x 128 KB
-    // = 35 MB of boundary rings (L2-resident) instead of 145 full rows (2.3 GB).
-    int64_t rb0 = 1;
-    while (rb0 < (int64_t)ncols) rb0 *= 2;
-    int64_t rb = 8192;
-    while (rb < 4 * ((int64_t)W * (32 + CHS) * C + chg + 64 * C)) rb *= 2;
-    if (const char* env = getenv("TWB_WAVE_RB")) {  // tuning experiments
-        const int64_t v = atoll(env);
-        if (v >= 1024 && (v & (v - 1)) == 0) rb = v;
-    }
-    if (rb > rb0) rb = rb0;
     std::vector<WaveArgs<R, Z>> args(nl);
     int64_t cta0 = 0;
     const int64_t pos_last = ((pr.nA - 1) / H) % G;  // ring position of the last stripe
@@ -277,15 +263,11 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
         a.p = pr.p;
         a.out = pt.out;
         const int64_t g = gp[live[l]];
-        a.rbmask = (int)(rb - 1);
-        a.rbmask0 = (int)(rb0 - 1);
-        const size_t slots = (size_t)(cta0 == 0 ? rb0 + (g - 1) * rb : g * rb);
-        a.gbuf = (Z*)pt.alloc.get(sizeof(Z) * slots);
-        a.gmbuf = (R*)pt.alloc.get(sizeof(R) * slots);
-        a.gprog = (long long*)pt.alloc.get(sizeof(long long) * 2 * (size_t)g);
+        a.gbuf = (Z*)pt.alloc.get(sizeof(Z) * (size_t)g * ncols);
+        a.gmbuf = (R*)pt.alloc.get(sizeof(R) * (size_t)g * ncols);
+        a.gprog = (long long*)pt.alloc.get(sizeof(long long) * (size_t)g);
         if (!a.gbuf || !a.gprog || !a.gmbuf) return cudaErrorMemoryAllocation;
-        a.gcons = a.gprog + g;
-        cudaError_t e = cudaMemsetAsync(a.gprog, 0, sizeof(long long) * 2 * (size_t)g, pt.st);
+        cudaError_t e = cudaMemsetAsync(a.gprog, 0, sizeof(long long) * (size_t)g, pt.st);
         if (e != cudaSuccess) return e;
         a.cta0 = cta0;
         a.GT = G;
@@ -309,7 +291,6 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
         args[l].next_z = nx.gbuf;
         args[l].next_m = nx.gmbuf;
         args[l].next_prog = nx.gprog;
-        args[l].next_cons = nx.gcons;
     }
     if (pr.gate == nullptr || pr.gate_want == 0) {  // the main sweep (not the gated NaN-exact one)
         ctx->wave_stripes = S;
@@ -430,13 +411,6 @@ cudaError_t run_wave_static(const WaveProblem<R, Z>& pr, const Alloc& alloc, cud
             if (c == "k4w16") return run_wave_cfg<D, 4, 1, P, E, N1, 16, 1, R, Z>(pr, alloc, st, ctx);
             if (c == "k8w12") return run_wave_cfg<D, 8, 1, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
             if (c == "k5w16") return run_wave_cfg<D, 5, 1, P, E, N1, 16, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k2w12") return run_wave_cfg<D, 2, 1, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k3w12") return run_wave_cfg<D, 3, 1, P, E, N1, 12, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k2w16") return run_wave_cfg<D, 2, 1, P, E, N1, 16, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k3w16") return run_wave_cfg<D, 3, 1, P, E, N1, 16, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k4w8") return run_wave_cfg<D, 4, 1, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
-            if (c == "k2w8x2") return run_wave_cfg<D, 2, 1, P, E, N1, 8, 2, R, Z>(pr, alloc, st, ctx);
-            if (c == "k3w8x2") return run_wave_cfg<D, 3, 1, P, E, N1, 8, 2, R, Z>(pr, alloc, st, ctx);
 #endif
             // C = 2 (two columns per lane step) measured within 3% of C = 1
             // on the B200 (profiles/r01_c2_variants.log): not instantiated.

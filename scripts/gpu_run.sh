@@ -49,6 +49,16 @@ if has ncu_wave; then
     > gpurun_out/${TAG}_ncu_wave.log 2>&1
   echo "ncu wave exit $?" >> gpurun_out/${TAG}_ncu_wave.log
 fi
+if has ncu_dram; then
+  # DRAM bytes + duration of the benchmarked cfg3 sweep and of the fused precompute (one launch each)
+  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    --kernel-name-base demangled -k "$K_WAVE" -c 1 --csv --log-file gpurun_out/${TAG}_wave_cfg3_dram.csv \
+    python scripts/prof_one.py cfg3 > gpurun_out/${TAG}_ncu_dram.log 2>&1
+  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
+    --kernel-name-base demangled -k regex:prepare_kernel -c 1 --csv --log-file gpurun_out/${TAG}_prepare_cfg3_dram.csv \
+    python scripts/prof_one.py cfg3 >> gpurun_out/${TAG}_ncu_dram.log 2>&1
+  echo "ncu dram exit $?" >> gpurun_out/${TAG}_ncu_dram.log
+fi
 if has ncu_wave_src; then
   # source-level counters on the same kernel configuration at n = 400k (one round of stripes)
   TWB_WAVE_CFG=k6w12 TWB_WAVE_WS=12 timeout 1200 ncu --set full --clock-control none --import-source on \
@@ -62,8 +72,8 @@ if has ncu_batch; then
   echo "ncu batch exit $?" >> gpurun_out/${TAG}_ncu_batch.log
 fi
 if has ncu_prep; then
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:prepare -c 2 \
-    -o gpurun_out/${TAG}_prepare_cfg3 -f python scripts/prof_one.py cfg3 --n 4000000 > gpurun_out/${TAG}_ncu_prep.log 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:prepare_kernel -c 1 \
+    -o gpurun_out/${TAG}_prepare_cfg3 -f python scripts/prof_one.py cfg3 > gpurun_out/${TAG}_ncu_prep.log 2>&1
   echo "ncu prep exit $?" >> gpurun_out/${TAG}_ncu_prep.log
 fi
 if [ -n "$EXTRA_CMD" ]; then
