@@ -224,7 +224,7 @@ int prepare_fused(const PrepIn<T, R, Z>* in, int nseg, int dim, double nu, doubl
         g.Del = in[k].Del;
         g.Vt = in[k].Vt;
         g.ldt = in[k].ntot + in[k].nseries;
-        g.tiles = (in[k].ntot + PREP_TILE - 1) / PREP_TILE;
+        g.tiles = (in[k].ntot + PREP_TILE * PREP_SPT - 1) / (PREP_TILE * PREP_SPT);
         tiles += g.tiles;
     }
     a.nseg = nseg;
@@ -239,12 +239,26 @@ int prepare_fused(const PrepIn<T, R, Z>* in, int nseg, int dim, double nu, doubl
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // ~35 KB of staging per CTA: 6 CTAs per SM keep ~1.5k tile loads in flight
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms * 6));
-    prepare_kernel<T, R, Z><<<(unsigned)grid, PREP_TILE, 0, st>>>(a);
-    ++t_launches;
-    CK(cudaGetLastError());
-    return 0;
+    a.staged = dim <= PREP_DMAX && (size_t)(PREP_TILE * PREP_SPT + 1) * dim * sizeof(T) + 32 <= 160 * 1024;
+    const size_t smem = a.staged ? (size_t)(PREP_TILE * PREP_SPT + 1) * dim * sizeof(T) + 32 : 0;
+    // 8 CTAs of 256 threads per SM (the thread limit) while the staging fits:
+    // each keeps one tile's bulk loads in flight
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms * 8));
+    auto go = [&](auto kern) -> int {
+        if (smem > 48 * 1024)
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<(unsigned)grid, PREP_TILE, smem, st>>>(a);
+        ++t_launches;
+        CK(cudaGetLastError());
+        return 0;
+    };
+    switch (dim) {
+        case 1: return go(prepare_kernel<T, R, Z, 1>);
+        case 2: return go(prepare_kernel<T, R, Z, 2>);
+        case 3: return go(prepare_kernel<T, R, Z, 3>);
+        case 4: return go(prepare_kernel<T, R, Z, 4>);
+    }
+    return go(prepare_kernel<T, R, Z, 0>);
 }
 template <typename T, typename R, typename Z>
 int prepare(const T* values, const T* times, const int64_t* d_off, int64_t nseries, int64_t ntot,

@@ -3,7 +3,7 @@
 // that picks the DP kernels' proven-safe or NaN-exact mode.
 //
 // One launch covers one or two segments (a pair's two series, or a packed
-// CSR list of series). A CTA takes tiles of PREP_TILE consecutive samples:
+// CSR list of series). A CTA takes tiles of PREP_TILE x PREP_SPT consecutive samples:
 // the tile's raw values and timestamps, plus the sample before it, are
 // staged in shared memory by bulk asynchronous copies (cp.async.bulk, TMA
 // engine, completion on an mbarrier; the < 16-byte unaligned head and tail of
@@ -14,8 +14,7 @@
 // with v_{-1} = 0, t_{-1} = 0 for a series' first sample (C:163-174), and
 // writes the prepared row o = i + k + 1 (sample i of series k); the series'
 // first sample also writes its virtual row o - 1 (V = virt, T = 0,
-// Del = +inf). V is written back as a flat, coalesced copy of the staged
-// values. The input check (every |x| < limit; fp values also 0 or >= tiny)
+// Del = +inf). The input check (every |x| < limit; fp values also 0 or >= tiny)
 // is a warp vote and one atomicOr per warp that finds a violation.
 //
 // Bound: HBM. Algorithmic bytes per sample: reads (d + 1) * sizeof(T),
@@ -27,8 +26,9 @@
 
 namespace twb {
 
-constexpr int PREP_TILE = 256;  // samples per tile = threads per CTA
-constexpr int PREP_DMAX = 16;   // staged dimensions (larger d: values read from global)
+constexpr int PREP_TILE = 256;  // threads per CTA
+constexpr int PREP_SPT = 4;     // samples per thread and tile (tile = 1024 samples)
+constexpr int PREP_DMAX = 64;   // staged dimensions (larger d: values read from global)
 
 template <typename T, typename R, typename Z>
 struct PrepSeg {
@@ -41,7 +41,7 @@ struct PrepSeg {
     Z* Del;              // (ntot + nseries)
     R* Vt;               // optional dim-major copy, leading dimension ldt
     int64_t ldt;
-    int64_t tiles;       // ceil(ntot / PREP_TILE)
+    int64_t tiles;       // ceil(ntot / (PREP_TILE * PREP_SPT))
 };
 
 template <typename T, typename R, typename Z>
@@ -54,6 +54,7 @@ struct PrepArgs {
     double virt;         // virtual row value: 0 (reference layout) or +inf (DP kernels' copy)
     double limit, tiny;  // input check: |x| < limit, and x == 0 or |x| >= tiny (values)
     int* flag;           // |= 1 when a check fails (null: no check)
+    int staged;          // values staged in (dynamic) shared memory
 };
 
 __device__ __forceinline__ double lp_rt(const double* x, const double* y, int d, int p) {
@@ -153,14 +154,49 @@ __device__ __forceinline__ bool value_bad(double a, double limit, double tiny) {
     return !(a < limit) || (a != 0.0 && a < tiny);
 }
 
-template <typename T, typename R, typename Z>
+// lp distance of sample i to sample i-1 (zero vector before a series' first
+// sample), lp_dist's operation order (_kernels.py:24-48); D > 0: compile-time
+// dimension (registers), D == 0: runtime d, read element by element.
+template <int D, typename GC, typename GP>
+__device__ __forceinline__ double consecutive_cost(GC cur, GP prev, bool first, int d, int p) {
+    if constexpr (D > 0) {
+        double x[D], y[D];
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            x[c] = cur(c);
+            y[c] = first ? 0.0 : prev(c);
+        }
+        return lp_rt(x, y, D, p);
+    } else {
+        if (d == 1) return fabs(cur(0) - (first ? 0.0 : prev(0)));
+        double acc = 0.0;
+        for (int c = 0; c < d; ++c) {
+            const double df = cur(c) - (first ? 0.0 : prev(c));
+            if (p == 1 || p == 2) {
+                const double term = p == 1 ? fabs(df) : __dmul_rn(df, df);
+                acc = c == 0 ? term : __dadd_rn(acc, term);
+            } else {
+                acc = __dadd_rn(acc, int_power(fabs(df), p));
+            }
+        }
+        return p == 1 ? acc : p == 2 ? __dsqrt_rn(acc) : pow(acc, 1.0 / (double)p);
+    }
+}
+
+// D: compile-time dimension (1..4) or 0 (runtime args.d). A tile is
+// PREP_TILE * PREP_SPT samples; thread t handles samples t, t + PREP_TILE, ...
+// of it (consecutive threads, consecutive samples: coalesced stores).
+// Dynamic shared memory: the staged values of a tile,
+// (PREP_TILE * PREP_SPT + 1) * d * sizeof(T) + 32 bytes, when args.staged
+// (else values are read from global memory).
+template <typename T, typename R, typename Z, int D>
 __global__ void __launch_bounds__(PREP_TILE) prepare_kernel(const PrepArgs<T, R, Z> args) {
-    // staged values: (PREP_TILE + 1) samples x PREP_DMAX, + 16 bytes of alignment slack
-    __shared__ __align__(16) unsigned char sv[(PREP_TILE + 1) * PREP_DMAX * sizeof(T) + 32];
-    __shared__ __align__(16) unsigned char st_[(PREP_TILE + 1) * sizeof(T) + 32];
+    constexpr int TS = PREP_TILE * PREP_SPT;
+    extern __shared__ __align__(16) unsigned char sv[];
+    __shared__ __align__(16) unsigned char st_[(TS + 1) * sizeof(T) + 32];
     __shared__ __align__(8) uint64_t bar;
-    const int d = args.d;
-    const bool staged_v = d <= PREP_DMAX;
+    const int d = D > 0 ? D : args.d;
+    const bool staged_v = args.staged != 0;
     if (threadIdx.x == 0) mbar_init(&bar, 1);
     __syncthreads();
     unsigned phase = 0;
@@ -168,8 +204,8 @@ __global__ void __launch_bounds__(PREP_TILE) prepare_kernel(const PrepArgs<T, R,
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int sg = tile < args.seg[0].tiles ? 0 : 1;
         const PrepSeg<T, R, Z>& S = args.seg[sg];
-        const int64_t i0 = (tile - (sg ? args.seg[0].tiles : 0)) * PREP_TILE;
-        const int64_t i1 = min(i0 + PREP_TILE, S.ntot);
+        const int64_t i0 = (tile - (sg ? args.seg[0].tiles : 0)) * TS;
+        const int64_t i1 = min(i0 + TS, S.ntot);
         const int64_t j0 = i0 > 0 ? i0 - 1 : 0;  // the sample before the tile
         __syncthreads();  // every thread is done with the previous tile's buffers
         if (threadIdx.x == 0) fence_proxy_async_smem();
@@ -182,56 +218,53 @@ __global__ void __launch_bounds__(PREP_TILE) prepare_kernel(const PrepArgs<T, R,
         __syncthreads();  // the threads' head / tail stores
         mbar_wait(&bar, phase);
         phase ^= 1;
-
-        const int64_t i = i0 + threadIdx.x;
+        // shared-memory views in element units: element e of the arrays sits at
+        // tv[e - j0] / vv[e - j0*d]
+        const T* tv = reinterpret_cast<const T*>(st_ + ((uintptr_t)(S.t + j0) - stt.base));
+        const T* vv = staged_v ? reinterpret_cast<const T*>(sv + ((uintptr_t)(S.v + j0 * d) - stv.base))
+                               : nullptr;
         bool bad = false;
-        if (i < i1) {
-            int64_t k;
-            if (S.uniform_n > 0) {
-                k = i / S.uniform_n;
-            } else {  // last k with off[k] <= i
-                int64_t lo = 0, hi = S.nseries;
-                while (hi - lo > 1) {
-                    const int64_t mid = (lo + hi) >> 1;
-                    if (S.off[mid] <= i) lo = mid; else hi = mid;
-                }
-                k = lo;
-            }
-            const int64_t start = S.uniform_n > 0 ? k * S.uniform_n : S.off[k];
-            const bool first = i == start;
-            const double ti = (double)stt.at(i);
-            const double tp = first ? 0.0 : (double)stt.at(i - 1);
-            bad |= args.flag && value_bad(ti, args.limit, 0.0);
-            double cost;
-            if (staged_v) {
-                double cur[PREP_DMAX], prev[PREP_DMAX];
-                for (int c = 0; c < d; ++c) {
-                    cur[c] = (double)stv.at(i * d + c);
-                    prev[c] = first ? 0.0 : (double)stv.at((i - 1) * d + c);
-                    bad |= args.flag && value_bad(cur[c], args.limit, args.tiny);
-                }
-                cost = lp_rt(cur, prev, d, args.p);
-            } else {  // long vectors: the same sums, read straight from memory
-                const T* x = S.v + i * d;
-                const T* y = S.v + (i - 1) * d;
-                double acc = 0.0;
-                for (int c = 0; c < d; ++c) {
-                    const double xc = (double)x[c];
-                    const double df = xc - (first ? 0.0 : (double)y[c]);
-                    bad |= args.flag && value_bad(xc, args.limit, args.tiny);
-                    if (args.p == 1 || args.p == 2) {
-                        const double term = args.p == 1 ? fabs(df) : __dmul_rn(df, df);
-                        acc = c == 0 ? term : __dadd_rn(acc, term);
-                    } else {
-                        acc = __dadd_rn(acc, int_power(fabs(df), args.p));
+#pragma unroll
+        for (int m = 0; m < PREP_SPT; ++m) {
+            const int64_t i = i0 + threadIdx.x + m * PREP_TILE;
+            if (i >= i1) break;
+            // series of sample i: one series (a pair's) -> 0; equal lengths ->
+            // a division (32-bit when it fits); ragged -> binary search
+            int64_t k = 0, start = 0;
+            if (S.nseries > 1) {
+                if (S.uniform_n > 0) {
+                    k = (S.ntot < (1ll << 31)) ? (int64_t)((unsigned)i / (unsigned)S.uniform_n)
+                                               : i / S.uniform_n;
+                    start = k * S.uniform_n;
+                } else {  // last k with off[k] <= i
+                    int64_t lo = 0, hi = S.nseries;
+                    while (hi - lo > 1) {
+                        const int64_t mid = (lo + hi) >> 1;
+                        if (S.off[mid] <= i) lo = mid; else hi = mid;
                     }
+                    k = lo;
+                    start = S.off[k];
                 }
-                cost = args.p == 1 ? acc : args.p == 2 ? __dsqrt_rn(acc) : pow(acc, 1.0 / (double)args.p);
             }
+            const bool first = i == start;
+            const int li = (int)(i - j0);  // position in the staged tile
+            const double ti = (double)tv[li];
+            const double tp = first ? 0.0 : (double)tv[li - 1];
+            bad |= args.flag && value_bad(ti, args.limit, 0.0);
+            const T* x = staged_v ? vv + (size_t)li * d : S.v + i * d;  // sample i
+            const T* y = x - d;                                         // sample i - 1
+            auto cur = [&](int c) { return (double)x[c]; };
+            auto prev = [&](int c) { return (double)y[c]; };
+            const double cost = consecutive_cost<D>(cur, prev, first, d, args.p);
+            if (args.flag)
+                for (int c = 0; c < d; ++c) bad |= value_bad(cur(c), args.limit, args.tiny);
             const double gap = fabs(ti - tp);
             const int64_t o = i + k + 1;
             S.Tm[o] = (R)ti;
             S.Del[o] = (Z)__dadd_rn(__dadd_rn(cost, __dmul_rn(args.nu, gap)), args.lam);  // core.py:233
+            for (int c = 0; c < d; ++c) S.V[o * d + c] = (R)x[c];
+            if (S.Vt)  // dim-major copy: consecutive threads, consecutive rows
+                for (int c = 0; c < d; ++c) S.Vt[c * S.ldt + o] = (R)x[c];
             if (first) {  // the series' virtual row o - 1
                 for (int c = 0; c < d; ++c) S.V[(o - 1) * d + c] = (R)args.virt;
                 if (S.Vt)
@@ -239,39 +272,9 @@ __global__ void __launch_bounds__(PREP_TILE) prepare_kernel(const PrepArgs<T, R,
                 S.Tm[o - 1] = R(0);
                 S.Del[o - 1] = (Z)dinf();
             }
-            if (S.Vt) {  // dim-major copy: consecutive threads, consecutive rows
-                for (int c = 0; c < d; ++c)
-                    S.Vt[c * S.ldt + o] = (R)(staged_v ? stv.at(i * d + c) : S.v[i * d + c]);
-            }
-            if (!staged_v)
-                for (int c = 0; c < d; ++c) S.V[o * d + c] = (R)S.v[i * d + c];
         }
         if (args.flag) {
             if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(args.flag, 1);
-        }
-        // V: the tile's staged values as one flat coalesced copy, shifted by
-        // the k + 1 rows of the series each sample belongs to
-        if (staged_v) {
-            const int64_t nel = (i1 - i0) * d;
-            int64_t kk = -1, kend = -1;
-            for (int64_t e = threadIdx.x; e < nel; e += PREP_TILE) {
-                const int64_t ii = i0 + e / d;
-                if (ii >= kend) {  // series of sample ii (threads move forward monotonically)
-                    if (S.uniform_n > 0) {
-                        kk = ii / S.uniform_n;
-                        kend = (kk + 1) * S.uniform_n;
-                    } else {
-                        int64_t lo = 0, hi = S.nseries;
-                        while (hi - lo > 1) {
-                            const int64_t mid = (lo + hi) >> 1;
-                            if (S.off[mid] <= ii) lo = mid; else hi = mid;
-                        }
-                        kk = lo;
-                        kend = S.off[kk + 1];
-                    }
-                }
-                S.V[(i0 + kk + 1) * d + e] = (R)stv.at(i0 * d + e);
-            }
         }
     }
 }

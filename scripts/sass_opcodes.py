@@ -53,8 +53,8 @@ def opcode(ins: str) -> str:
 
 
 def hot_loop(ins, arith):
-    """The innermost loop (no backward branch nested in its body) with the
-    most arithmetic instructions."""
+    """The steady-state loop: among the innermost loops (no backward branch
+    nested in their body), the densest in arithmetic."""
     loops = []
     for a, s in ins:
         if "BRA" not in s:
@@ -64,13 +64,18 @@ def hot_loop(ins, arith):
             loops.append((int(t.group(1), 16), a))
     inner = [(lo, hi) for lo, hi in loops
              if not any(lo <= l2 and h2 < hi and (l2, h2) != (lo, hi) for l2, h2 in loops)]
-    best = None
+    cand = []
     for lo, hi in inner:
         body = [x for x in ins if lo <= x[0] <= hi]
         n = sum(1 for _, x in body if re.search(arith, x))
-        if n and (best is None or n > best[0]):
-            best = (n, body)
-    return best[1] if best else []
+        if n:
+            cand.append((n, body))
+    if not cand:
+        return []
+    # the steady state: the densest of the loops carrying at least half the
+    # largest loop's arithmetic (the pipeline fill is a bigger, sparser loop)
+    top = max(n for n, _ in cand)
+    return max(((n / len(b), b) for n, b in cand if n >= top / 2), key=lambda t: t[0])[1]
 
 
 def main():
