@@ -245,7 +245,8 @@ int prepare_fused(const PrepIn<T, R, Z>* in, int nseg, int dim, double nu, doubl
     // each keeps one tile's bulk loads in flight
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms * 8));
     auto go = [&](auto kern) -> int {
-        if (smem > 48 * 1024)
+        // static staging (times, ~8 KB) + dynamic: opt in above 32 KB of dynamic
+        if (smem > 32 * 1024)
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<(unsigned)grid, PREP_TILE, smem, st>>>(a);
         ++t_launches;

@@ -63,7 +63,15 @@ struct BatchArgs {
 
 // Lanes per A series: 16 when every row-side series has <= 128 samples (two
 // series per warp share one staged B stream), else 32.
-__host__ __device__ constexpr int batch_lanes(int64_t max_rows) { return max_rows <= 128 ? 16 : 32; }
+// TWB_BATCH_LW8: series of <= 32 samples get 8 lanes x 4 rows (four series per
+// warp) instead of 16 x 2: twice the rows per lane (more independent work per
+// loaded column value) and half the lane skew.
+#ifndef TWB_BATCH_LW8
+#define TWB_BATCH_LW8 1
+#endif
+__host__ __device__ constexpr int batch_lanes(int64_t max_rows) {
+    return (TWB_BATCH_LW8 && max_rows <= 32) ? 8 : max_rows <= 128 ? 16 : 32;
+}
 
 // One warp per task = (row group, run of `chunk` B series). A row group is
 // 32/LW consecutive A series (LW lanes each, K rows per lane, rows in
@@ -200,7 +208,9 @@ __global__ void __launch_bounds__(WARPS * 32) batch_kernel(const BatchArgs<R, Z>
             // column j with the distances + prep of column j+1, as in
             // wave_kernel) with predicated series bookkeeping; the drain runs
             // the same body lane-predicated.
-            for (; s < min(LW, nsteps); ++s) generic(s);
+            // (at least 16 steps: the 16-step groups below must start at a
+            // multiple of 16 for the every-32-steps column staging)
+            for (; s < min(LW > 16 ? LW : 16, nsteps); ++s) generic(s);
             if (s < nsteps) {
                 Z pre[K];
                 R tbj;

@@ -124,6 +124,7 @@ cudaError_t run_batch(BatchArgs<R, Z> a, int64_t max_rows, const Alloc& alloc, c
         ctx->after(st);
         return cudaGetLastError();
     };
+    if (batch_lanes(max_rows) == 8) return go(batch_kernel<D, 4, 8, P, E, N1, BATCH_WARPS, R, Z>, 4);
     if (max_rows <= 16 * 2) return go(batch_kernel<D, 2, 16, P, E, N1, BATCH_WARPS, R, Z>, 2);
     if (max_rows <= 16 * 4) return go(batch_kernel<D, 4, 16, P, E, N1, BATCH_WARPS, R, Z>, 4);
     if (max_rows <= 16 * 8) return go(batch_kernel<D, 8, 16, P, E, N1, BATCH_WARPS, R, Z>, 8);
