@@ -683,7 +683,7 @@ int twed_batch_dev_impl(const T* dAA, const int64_t* a_off, int64_t nAA, const T
     }
     // runtime-d kernels read the columns (the B side) dim-major
     R* VtB = use_dyn(dim) ? sc.get_n<R>((totB + nBB) * dim) : nullptr;
-    const int64_t ldtB = totB + nBB;
+    [[maybe_unused]] const int64_t ldtB = totB + nBB;
     if (sc.failed) return fail(TWB_ENOMEM, "device scratch allocation failed");
     CK(cudaMemsetAsync(dflag, 0, sizeof(int), st));
     CK(cudaMemcpyAsync(d_aoff, a_off, sizeof(int64_t) * (nAA + 1), cudaMemcpyHostToDevice, st));

@@ -71,8 +71,11 @@ def sharded_batch(n_rows: int, n_cols: int, tri: bool,
     import torch
     import torch.distributed as dist
 
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
+    if not dist.is_initialized():  # one process, no process group: the whole matrix here
+        world, rank = 1, 0
+    else:
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
     bounds = row_bounds(n_rows, world, tri)
     b0, b1 = bounds[rank]
     if dtype is None:
@@ -112,7 +115,8 @@ def sharded_batch(n_rows: int, n_cols: int, tri: bool,
 def twed_batch_distributed(AA, TAA=None, BB=None, TBB=None, nu=1.0, lamb=None, degree=2,
                            tri=False, *, lam=None, dtype=None, group=None):
     """twed_batch over every rank of the default process group (one GPU each,
-    LOCAL_RANK = device). Returns the full numpy matrix on rank 0, None elsewhere."""
+    LOCAL_RANK = device). Returns the full numpy matrix on rank 0, None elsewhere
+    (without a process group: the whole matrix on the current device)."""
     import torch
 
     from .api import _dtype, _lam, _to_list, batch_matrix
