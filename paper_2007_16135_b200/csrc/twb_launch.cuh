@@ -239,12 +239,15 @@ cudaError_t run_wave_cfg(const WaveProblem<R, Z>& pr, const Alloc& alloc, cudaSt
         if (gp[q] > 0) live.push_back(q);
     const int nl = (int)live.size();
     // Bottom-row publish granularity: every st.release.gpu costs the
-    // producing warp a GPU-scope fence, so publish every chg columns (more for
-    // long rows; the consumer lags far behind anyway). TWB_WAVE_CHG overrides.
+    // producing warp a GPU-scope fence, but a coarse publish leaves the next
+    // CTA waiting for data that exists, and its stalls travel down the chain.
+    // B200 sweep (profiles/r02_wave_ab.log, r02I): 32 columns is best or tied
+    // everywhere -- n = 1M d = 3 490.0 vs 484.9 GCUPS at the former 256,
+    // n = 300k d = 3 420.6 vs 387.8, 1024 costs 3.4 %, 4096 15 %.
+    // TWB_WAVE_CHG overrides.
     int chg = 32;
-    while (chg < 256 && (int64_t)chg * 2048 <= pr.nB) chg *= 2;
     if (const char* env = getenv("TWB_WAVE_CHG")) chg = atoi(env);
-    if (chg < 32 || (chg & (chg - 1))) chg = 32;
+    if (chg < CHS || (chg & (chg - 1))) chg = 32;
     const size_t ncols = (size_t)(pr.nB + 1);
     std::vector<WaveArgs<R, Z>> args(nl);
     int64_t cta0 = 0;
