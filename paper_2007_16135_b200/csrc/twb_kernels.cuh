@@ -311,13 +311,23 @@ __host__ __device__ constexpr size_t wave_smem_rings(int warps) {
 #ifndef TWB_WAVE_SA
 #define TWB_WAVE_SA -1
 #endif
-template <int D, typename R>
+// K = 8 keeps its rows in registers: the K = 8 build with rows in shared
+// memory and the pipelined fill returned nondeterministic distances (+2432
+// exactly at d = 3, +2304 at d = 2, any n, 8 active warps; round 2 race hunt,
+// profiles/r02_wave_ab.log) that neither the rows-in-registers nor the
+// generic-fill build shows; the root cause is not found, the combination is
+// not built.
+#ifndef TWB_WAVE_SA_K8
+#define TWB_WAVE_SA_K8 0
+#endif
+template <int D, typename R, int K = 6>
 __host__ __device__ constexpr bool wave_sa() {
+    if (K >= 8 && !TWB_WAVE_SA_K8) return false;
     return TWB_WAVE_SA < 0 ? (D >= 2 && sizeof(R) == 8) : TWB_WAVE_SA != 0;
 }
 template <int D, typename R, int K>
 __host__ __device__ constexpr size_t wave_smem_rows(int warps) {
-    return wave_sa<D, R>() ? (size_t)warps * 32 * K * RowChunks<D, R>::BYTES_PER_LANE_ROW : 0;
+    return wave_sa<D, R, K>() ? (size_t)warps * 32 * K * RowChunks<D, R>::BYTES_PER_LANE_ROW : 0;
 }
 template <int D, typename R, typename Z, int C>
 __host__ __device__ constexpr size_t wave_smem_base(int warps) {  // 16-aligned
@@ -377,7 +387,7 @@ __device__ __forceinline__ long long globaltimer() {
 template <int D, int K, int C, int P, bool EXACT_NAN, bool NU1, int WARPS, int MINB, typename R,
           typename Z>
 __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R, Z> args) {
-    using Lane = LaneRows<D, K, P, EXACT_NAN, NU1, R, Z, wave_sa<D, R>()>;
+    using Lane = LaneRows<D, K, P, EXACT_NAN, NU1, R, Z, wave_sa<D, R, K>()>;
     using Ring = WaveRing<D, R, Z, C>;
     constexpr int NC = Ring::N;
     constexpr int GCOLS = C * CHS;  // columns per group of CHS steps
@@ -418,7 +428,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
         L.dd = args.dd;
         L.sa = (args.arows ? args.arows + ((size_t)b * WARPS + warp) * blk : srows + (size_t)warp * blk) +
                lane;
-    } else if constexpr (wave_sa<D, R>()) {
+    } else if constexpr (wave_sa<D, R, K>()) {
         L.sa = srows + ((size_t)warp * K * Lane::RC::NCH * 32 + lane) * Lane::RC::EPC;
     }
 
