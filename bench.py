@@ -2,15 +2,19 @@
 """Benchmark of the TWED hot path on B200 (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload cfg3|cfg3_f32|cfg2|cfg1] [--no-batch] [--no-cpu]
+                    [--workload cfg3|cfg3_f32|cfg2|cfg1|cfg5] [--no-batch] [--no-cpu]
 
 Headline (N=1): BASELINE.json's metric "TWED GCUPS at the n=1M pair" on
 config 3 (single pair, 3-D random walks, n = 1,000,000, nu = 1, lam = 1,
 degree 2, fp64). One step = one full distance of the pair (1e12 DP cells).
-The single pair does not shard across GPUs (replicas only),
-so with N > 1 every rank solves its own replica (weak scaling). The batch
-half of the metric -- twed_batch pairs/s on the 10k x 10k tri config 5 --
-is reported in the "batch" object, sharded over the N GPUs (strong scaling).
+The single pair does not shard across GPUs, so with N > 1
+(torchrun) the headline becomes the batch half of the metric -- twed_batch
+pairs/s on the 10k x 10k tri config 5, strong-scaled over the ranks, the
+unpadded gather to rank 0 and the on-device mirror inside the timed region
+(--workload cfg5 selects it at any N). At N = 1 the batch is reported in the
+"batch" object, and "other_configs" carries the other BASELINE configs, the
+precompute's HBM GB/s, config 1's host-call latency, batch e2e (numpy in and
+out), the paper's R^28 batch shape and LCS.
 
   value  : whole-job GCUPS with inputs resident in HBM (device API, CUDA
            events on the launching stream, max over ranks).
