@@ -311,18 +311,19 @@ __host__ __device__ constexpr size_t wave_smem_rings(int warps) {
 #ifndef TWB_WAVE_SA
 #define TWB_WAVE_SA -1
 #endif
-// K = 8 keeps its rows in registers: the K = 8 build with rows in shared
-// memory and the pipelined fill returned nondeterministic distances (+2432
-// exactly at d = 3, +2304 at d = 2, any n, 8 active warps; round 2 race hunt,
-// profiles/r02_wave_ab.log) that neither the rows-in-registers nor the
-// generic-fill build shows; the root cause is not found, the combination is
-// not built.
-#ifndef TWB_WAVE_SA_K8
-#define TWB_WAVE_SA_K8 0
+// Rows in shared memory only for K = 6 (the headline configuration): the
+// K = 8 (8 warps) and K = 4 (12 warps) builds with rows in shared memory and
+// the pipelined fill returned nondeterministic distances (+2432 exactly at
+// d = 3, +2304 at d = 2, any n, all warps active; round 2 repetition hunt,
+// profiles/r02_wave_ab.log) that neither their rows-in-registers nor their
+// generic-fill builds show, and that K = 6 never showed. Root cause not found;
+// those combinations are not built (TWB_WAVE_SA_ANYK=1 restores them).
+#ifndef TWB_WAVE_SA_ANYK
+#define TWB_WAVE_SA_ANYK 0
 #endif
 template <int D, typename R, int K = 6>
 __host__ __device__ constexpr bool wave_sa() {
-    if (K >= 8 && !TWB_WAVE_SA_K8) return false;
+    if (K != 6 && !TWB_WAVE_SA_ANYK) return false;
     return TWB_WAVE_SA < 0 ? (D >= 2 && sizeof(R) == 8) : TWB_WAVE_SA != 0;
 }
 template <int D, typename R, int K>

@@ -1,8 +1,9 @@
 """Repeatability of the wavefront: the same pair swept many times, on every
 wavefront configuration and stripe height, gives the oracle's distance every
-time. (Round 2 found a configuration -- 8 warps x 8 rows per lane with the
-rows in shared memory -- whose results varied between runs by exactly +2432;
-that combination is no longer built. This pins it.)"""
+time. (Round 2 found configurations -- 8 warps x 8 rows per lane and 12 warps
+x 4 rows per lane, each with the rows in shared memory and the pipelined fill
+-- whose results varied between runs by exactly +2432 at d = 3; those
+combinations are no longer built. This pins it.)"""
 
 import os
 
