@@ -311,19 +311,8 @@ __host__ __device__ constexpr size_t wave_smem_rings(int warps) {
 #ifndef TWB_WAVE_SA
 #define TWB_WAVE_SA -1
 #endif
-// Rows in shared memory only for K = 6 (the headline configuration): the
-// K = 8 (8 warps) and K = 4 (12 warps) builds with rows in shared memory and
-// the pipelined fill returned nondeterministic distances (+2432 exactly at
-// d = 3, +2304 at d = 2, any n, all warps active; round 2 repetition hunt,
-// profiles/r02_wave_ab.log) that neither their rows-in-registers nor their
-// generic-fill builds show, and that K = 6 never showed. Root cause not found;
-// those combinations are not built (TWB_WAVE_SA_ANYK=1 restores them).
-#ifndef TWB_WAVE_SA_ANYK
-#define TWB_WAVE_SA_ANYK 0
-#endif
 template <int D, typename R, int K = 6>
 __host__ __device__ constexpr bool wave_sa() {
-    if (K != 6 && !TWB_WAVE_SA_ANYK) return false;
     return TWB_WAVE_SA < 0 ? (D >= 2 && sizeof(R) == 8) : TWB_WAVE_SA != 0;
 }
 template <int D, typename R, int K>
@@ -687,6 +676,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
 #pragma unroll
             for (int q = 0; q < K; ++q) pre[q] = INF;
             R tbj = L.tbp;
+            // the column staging of [0, 64C) was only issued: without this
+            // wait the pipelined fill's first prep (lane 0, column 0) can read
+            // the slot's previous stripe (nondeterministic +2432 at d = 3)
+            cp_async_wait<0>();
+            __syncwarp();
             if (C * (st - lane) >= 0) {
                 const int j = C * (st - lane);
                 const int slot = j & (NC - 1);

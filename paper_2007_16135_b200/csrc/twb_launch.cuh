@@ -435,8 +435,9 @@ cudaError_t run_wave_static(const WaveProblem<R, Z>& pr, const Alloc& alloc, cud
         //   d = 1 : 100k 332 vs 357 vs 334; 300k 710 vs 679 vs 667
         //   d = 2 : 100k  84 vs 238 vs 201; 300k 233 vs 366 vs 385
         const int64_t n = pr.nA;
-        // round 2 (K = 8 rows now in registers, see wave_sa): d = 3 100k 178.9
-        // (k8w8) vs 207.7 (k6w12) GCUPS, 300k 402.0 vs 358.2, 600k 463.6 vs 425.0
+        // round 2: d = 3 100k 178.9 (k8w8) vs 207.7 (k6w12) GCUPS, 300k 402.0
+        // vs 358.2, 600k 463.6 vs 425.0 (K = 8 rows in registers); 300k 414.1
+        // with the rows in shared memory again (after the staging-wait fix)
         if (D >= 3 && n >= (int64_t)sms * 1350 && n < (int64_t)sms * 5400)
             return run_wave_cfg<D, 8, 1, P, E, N1, 8, 1, R, Z>(pr, alloc, st, ctx);
         if (D >= 3 && n >= (int64_t)sms * 150 && n < (int64_t)sms * 1350)

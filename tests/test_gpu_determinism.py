@@ -1,9 +1,9 @@
 """Repeatability of the wavefront: the same pair swept many times, on every
 wavefront configuration and stripe height, gives the oracle's distance every
 time. (Round 2 found configurations -- 8 warps x 8 rows per lane and 12 warps
-x 4 rows per lane, each with the rows in shared memory and the pipelined fill
--- whose results varied between runs by exactly +2432 at d = 3; those
-combinations are no longer built. This pins it.)"""
+x 4 rows per lane with the pipelined fill -- whose results varied between runs
+by exactly +2432 at d = 3: the fill's first prep read the column ring before
+the stripe's column staging had landed. This pins the fix.)"""
 
 import os
 
