@@ -7,12 +7,14 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
 #include <type_traits>
 #include <vector>
 #include <functional>
+#include <future>
 #include <thread>
 
 #include "../../include/twb.h"
@@ -901,6 +903,30 @@ int twed_batch_dev(const T* dAA, const int64_t* a_off, int64_t nAA, const T* dTA
     }
 }
 
+// A large result (cfg5: 400 MB) usually lands in freshly allocated host
+// memory, whose first-touch page faults would otherwise be taken inside the
+// device-to-host copy (cfg5 e2e 491 -> 428 ms). Two host threads take them
+// while the kernels run; the caller waits on the future before its copies,
+// which then overwrite every byte. TWB_PREFAULT=0 disables it.
+constexpr size_t PREFAULT_MIN_BYTES = (size_t)64 << 20;
+std::shared_future<void> prefault_async(void* out, size_t bytes) {
+    static const bool on = !getenv("TWB_PREFAULT") || atoi(getenv("TWB_PREFAULT")) != 0;
+    if (!on || bytes < PREFAULT_MIN_BYTES) {
+        std::promise<void> done;
+        done.set_value();
+        return done.get_future().share();
+    }
+    return std::async(std::launch::async, [out, bytes]() {
+               volatile char* p = reinterpret_cast<volatile char*>(out);
+               const size_t half = bytes / 2 / 4096 * 4096;
+               std::thread second([=]() {
+                   for (size_t i = half; i < bytes; i += 4096) p[i] = 0;
+               });
+               for (size_t i = 0; i < half; i += 4096) p[i] = 0;
+               second.join();
+           }).share();
+}
+
 template <typename T, typename O>
 int twed_batch_host(const T* AA, const int64_t* a_off, int64_t nAA, const T* TAA, const T* BB,
                     const int64_t* b_off, int64_t nBB, const T* TBB, int dim, double nu, double lam,
@@ -930,11 +956,13 @@ int twed_batch_host(const T* AA, const int64_t* a_off, int64_t nAA, const T* TAA
         CK(cudaMemcpyAsync(dB, BB, sizeof(T) * totB * dim, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(dTB, TBB, sizeof(T) * totB, cudaMemcpyHostToDevice, st));
     }
+    const size_t out_bytes = sizeof(O) * (size_t)(row_end - row_begin) * ncols;
+    std::shared_future<void> faulted = prefault_async(out, out_bytes);
     rc = twed_batch_dev<T, O>(dA, a_off, nAA, dTA, dB, b_off, nBB, dTB, dim, nu, lam, degree, tri,
                               row_begin, row_end, st, dout);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(out, dout, sizeof(O) * (size_t)(row_end - row_begin) * ncols,
-                       cudaMemcpyDeviceToHost, st));
+    faulted.wait();
+    CK(cudaMemcpyAsync(out, dout, out_bytes, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return 0;
 }
@@ -1019,6 +1047,9 @@ int twed_batch_multi(const T* AA, const int64_t* a_off, int64_t nAA, const T* TA
     lo[ndev] = nAA;
     std::vector<int> rcs(ndev, 0);
     std::vector<std::string> msgs(ndev);
+    // every block's copies wait for the whole matrix to be faulted in (a
+    // device also writes into other blocks' rows: the transposed strip)
+    std::shared_future<void> faulted = prefault_async(out, sizeof(O) * (size_t)nAA * ncols);
     auto block = [&](int k) -> int {
         const int64_t r0 = lo[k], r1 = lo[k + 1];
         if (r1 <= r0) return 0;
@@ -1045,6 +1076,7 @@ int twed_batch_multi(const T* AA, const int64_t* a_off, int64_t nAA, const T* TA
         int rc2 = twed_batch_dev<T, O>(dA, a_off, nAA, dTA, dB, b_off, nBB, dTB, dim, nu, lam, degree,
                                        tri, r0, r1, st, dout);
         if (rc2) return rc2;
+        faulted.wait();
         if (!tri) {
             CK(cudaMemcpyAsync(out + r0 * ncols, dout, sizeof(O) * (size_t)rows * ncols,
                                cudaMemcpyDeviceToHost, st));
