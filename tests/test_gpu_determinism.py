@@ -47,3 +47,26 @@ def test_repeated_sweeps_equal_the_oracle(twb, oracle, cfg, ws, d):
             else:
                 os.environ[k] = v
     assert all(g == want for g in got), (cfg, ws, d, sorted(set(got)), want)
+
+
+def test_repeated_mid_size_sweeps_agree(twb):
+    """n = 300k, d = 3, 8 warps x 8 rows: the shape that showed the +2432 in
+    nearly every batch of 6 sweeps before the fix (too large for the oracle in
+    a test; compared with the 12-warp x 6-row sweep, which never showed it)."""
+    import torch
+    from paper_2007_16135_b200.workloads import make_pair
+    dev = torch.device("cuda:0")
+    t = [torch.from_numpy(np.ascontiguousarray(x)).to(dev) for x in make_pair(300_000, 3, 2)]
+    old = {k: os.environ.get(k) for k in ("TWB_WAVE_CFG", "TWB_WAVE_WS")}
+    try:
+        os.environ["TWB_WAVE_CFG"], os.environ["TWB_WAVE_WS"] = "k6w12", "0"
+        want = twb.twed_dev(*t, nu=1.0, lamb=1.0, degree=2).item()
+        os.environ["TWB_WAVE_CFG"], os.environ["TWB_WAVE_WS"] = "k8w8", "8"
+        got = [twb.twed_dev(*t, nu=1.0, lamb=1.0, degree=2).item() for _ in range(8)]
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    assert all(g == want for g in got), (sorted(set(got)), want)
