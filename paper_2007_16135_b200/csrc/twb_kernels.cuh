@@ -291,7 +291,10 @@ constexpr int WAVE_UNROLL = TWB_WAVE_UNROLL;
 #define TWB_DBG_NOSYNC 0
 #endif
 constexpr int ZRS = 256;  // shared-memory ring between consecutive warps (columns)
-constexpr int CHS = 16;   // warp-to-warp publish granularity (columns)
+#ifndef TWB_CHS
+#define TWB_CHS 16
+#endif
+constexpr int CHS = TWB_CHS;  // warp-to-warp publish granularity (columns); divides 32
 constexpr int CHG = 32;   // CTA-to-CTA read granularity (columns; publish = args.chg)
 constexpr int CHG_RAMP = 4096;  // publish every group for the first columns of a stripe
 
@@ -748,8 +751,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
             while (C * (st + CHS) < ncols) {
                 const int st0 = st;
                 preamble(st);
-                if (to_ring) {  // lane 31 writes columns < C*(st0 - 15) this group
-                    const int need = C * (st0 - 15) - ZRS;
+                if (to_ring) {  // lane 31 writes columns < C*(st0 + CHS - 31) this group
+                    const int need = C * (st0 + CHS - 31) - ZRS;
                     while (TWB_DBG_NOSYNC < 2 && ld_acquire_cta(&cons[warp + 1]) < need &&
                            !s_abort_seen())
                         spin_pause();
