@@ -290,7 +290,10 @@ constexpr int WAVE_UNROLL = TWB_WAVE_UNROLL;
 #ifndef TWB_DBG_NOSYNC
 #define TWB_DBG_NOSYNC 0
 #endif
-constexpr int ZRS = 256;  // shared-memory ring between consecutive warps (columns)
+#ifndef TWB_ZRS
+#define TWB_ZRS 256
+#endif
+constexpr int ZRS = TWB_ZRS;  // shared-memory ring between consecutive warps (columns; power of 2)
 #ifndef TWB_CHS
 #define TWB_CHS 16
 #endif
@@ -318,14 +321,25 @@ template <int D, typename R, int K = 6>
 __host__ __device__ constexpr bool wave_sa() {
     return TWB_WAVE_SA < 0 ? (D >= 2 && sizeof(R) == 8) : TWB_WAVE_SA != 0;
 }
+// Warp-ring size: 512 columns where the rows sit in registers (d = 1, fp32
+// mode: shared memory to spare; more slack between neighbouring warps, n = 100k
+// d = 1 364 vs 357 GCUPS), 256 where the rows take the shared memory.
+#ifndef TWB_ZRS_REG
+#define TWB_ZRS_REG 512
+#endif
+template <int D, typename R>
+__host__ __device__ constexpr int wave_zrs() {
+    return (D >= 1 && !wave_sa<D, R>()) ? TWB_ZRS_REG : TWB_ZRS;
+}
 template <int D, typename R, int K>
 __host__ __device__ constexpr size_t wave_smem_rows(int warps) {
     return wave_sa<D, R, K>() ? (size_t)warps * 32 * K * RowChunks<D, R>::BYTES_PER_LANE_ROW : 0;
 }
 template <int D, typename R, typename Z, int C>
 __host__ __device__ constexpr size_t wave_smem_base(int warps) {  // 16-aligned
-    return (wave_smem_rings<D, R, Z, C>(warps) + sizeof(Z) * (ZRS * warps + ZRS) +
-            sizeof(R) * (ZRS * warps + ZRS) + sizeof(int) * 2 * warps + 15) / 16 * 16;
+    constexpr size_t zrs = wave_zrs<D, R>();
+    return (wave_smem_rings<D, R, Z, C>(warps) + sizeof(Z) * (zrs * warps + zrs) +
+            sizeof(R) * (zrs * warps + zrs) + sizeof(int) * 2 * warps + 15) / 16 * 16;
 }
 template <int D, typename R, typename Z, int C, int K>
 __host__ __device__ constexpr size_t wave_smem(int warps) {
@@ -384,6 +398,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
     using Ring = WaveRing<D, R, Z, C>;
     constexpr int NC = Ring::N;
     constexpr int GCOLS = C * CHS;  // columns per group of CHS steps
+    constexpr int ZRS = wave_zrs<D, R>();  // this configuration's warp-ring size
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto* rings = reinterpret_cast<Ring*>(smem_raw);
     unsigned char* p0 = smem_raw + wave_smem_rings<D, R, Z, C>(WARPS);
