@@ -281,10 +281,15 @@ __device__ __forceinline__ void spin_pause() {
 
 // Steady-state steps per loop iteration: unrolling lets the scheduler overlap
 // one step's latency-bound z chain with the next step's distance arithmetic.
+// 2 where the rows sit in shared memory (fp64 d >= 2: n = 1M d = 3 490 vs
+// 483 GCUPS at 4), 4 where they sit in registers (n = 100k d = 1 383 vs 364,
+// 1M d = 1 +0.9 %, fp32 mode +0.6 %; profiles/r02_wave_ab.log).
 #ifndef TWB_WAVE_UNROLL
 #define TWB_WAVE_UNROLL 2
 #endif
-constexpr int WAVE_UNROLL = TWB_WAVE_UNROLL;
+#ifndef TWB_WAVE_UNROLL_REG
+#define TWB_WAVE_UNROLL_REG 4
+#endif
 // Timing experiments only (results are wrong): 1 = CTAs do not wait for the
 // previous stripe's boundary row, 2 = warps do not wait for each other either.
 #ifndef TWB_DBG_NOSYNC
@@ -399,6 +404,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
     constexpr int NC = Ring::N;
     constexpr int GCOLS = C * CHS;  // columns per group of CHS steps
     constexpr int ZRS = wave_zrs<D, R>();  // this configuration's warp-ring size
+    constexpr int UNROLL = (D >= 1 && !wave_sa<D, R>()) ? TWB_WAVE_UNROLL_REG : TWB_WAVE_UNROLL;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     auto* rings = reinterpret_cast<Ring*>(smem_raw);
     unsigned char* p0 = smem_raw + wave_smem_rings<D, R, Z, C>(WARPS);
@@ -775,7 +781,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) wave_kernel(const WaveArgs<R
                 if (st0 < 32) {
                     for (int i = 0; i < CHS; ++i) body(st0 + i, false, true);
                 } else {
-#pragma unroll WAVE_UNROLL
+#pragma unroll UNROLL
                     for (int i = 0; i < CHS; ++i) body(st0 + i, false, false);
                 }
                 st += CHS;
