@@ -282,13 +282,14 @@ __device__ __forceinline__ void spin_pause() {
 // Steady-state steps per loop iteration: unrolling lets the scheduler overlap
 // one step's latency-bound z chain with the next step's distance arithmetic.
 // 2 where the rows sit in shared memory (fp64 d >= 2: n = 1M d = 3 490 vs
-// 483 GCUPS at 4), 4 where they sit in registers (n = 100k d = 1 383 vs 364,
-// 1M d = 1 +0.9 %, fp32 mode +0.6 %; profiles/r02_wave_ab.log).
+// 483 GCUPS at 4), 8 where they sit in registers (vs 2: n = 100k d = 1 401 vs
+// 364, 300k d = 1 845 vs 795, 1M d = 1 +1.6 %, fp32 mode +1.4 %; 16 is slower;
+// profiles/r02_wave_ab.log).
 #ifndef TWB_WAVE_UNROLL
 #define TWB_WAVE_UNROLL 2
 #endif
 #ifndef TWB_WAVE_UNROLL_REG
-#define TWB_WAVE_UNROLL_REG 4
+#define TWB_WAVE_UNROLL_REG 8
 #endif
 // Timing experiments only (results are wrong): 1 = CTAs do not wait for the
 // previous stripe's boundary row, 2 = warps do not wait for each other either.
